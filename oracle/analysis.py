@@ -1,0 +1,57 @@
+"""Titration analysis.
+
+* frame classification: deprotonated iff lambda_p >= 0.5 (reading R1)
+* x = N_deprot / N per (pH, replica)
+* H-H fit x(pH) = 1/(10^(pKa - pH) + 1) and Hill fit 1/(10^(n(pKa - pH)) + 1) by
+  SciPy non-linear least squares, unweighted over all
+  (pH, replica) points
+* bootstrap: per pH resample R replica fractions with replacement, refit,
+  5000 times, percentile 95% CI
+"""
+import numpy as np
+from scipy.optimize import least_squares
+
+
+def deprotonated_fraction(lp_frames):
+    lp = np.asarray(lp_frames, np.float64)
+    if not np.all(np.isfinite(lp)):
+        raise ValueError("non-finite lambda")
+    return float(np.mean(lp >= 0.5))
+
+
+def hh(pH, pKa, n=1.0):
+    return 1.0 / (10.0 ** (n * (pKa - np.asarray(pH, np.float64))) + 1.0)
+
+
+def fit_hh(pH, x):
+    pH = np.asarray(pH, np.float64)
+    x = np.asarray(x, np.float64)
+    p0 = pH[np.argmin(np.abs(x - 0.5))]
+    r = least_squares(lambda v: hh(pH, v[0]) - x, [p0], xtol=1e-15, ftol=1e-15, gtol=1e-15)
+    return float(r.x[0])
+
+
+def fit_hill(pH, x):
+    pH = np.asarray(pH, np.float64)
+    x = np.asarray(x, np.float64)
+    p0 = pH[np.argmin(np.abs(x - 0.5))]
+    r = least_squares(lambda v: hh(pH, v[0], v[1]) - x, [p0, 1.0], xtol=1e-15, ftol=1e-15, gtol=1e-15)
+    return float(r.x[0]), float(r.x[1])
+
+
+def bootstrap(pH_levels, fractions, B=5000, seed=0, hill=False):
+    """fractions: (n_pH, R).  Returns (estimate, lo, hi) of pKa (and n if hill)."""
+    rng = np.random.default_rng(seed)
+    f = np.asarray(fractions, np.float64)
+    npH, R = f.shape
+    pHs = np.repeat(np.asarray(pH_levels, np.float64), R)
+    est = fit_hill(pHs, f.reshape(-1)) if hill else fit_hh(pHs, f.reshape(-1))
+    draws = []
+    for _ in range(B):
+        idx = rng.integers(0, R, size=(npH, R))
+        fr = np.take_along_axis(f, idx, 1).reshape(-1)
+        draws.append(fit_hill(pHs, fr) if hill else fit_hh(pHs, fr))
+    d = np.array(draws)
+    lo = np.percentile(d, 2.5, axis=0)
+    hi = np.percentile(d, 97.5, axis=0)
+    return est, lo, hi
