@@ -1,0 +1,209 @@
+/*
+ * cph.h — C ABI of the B200 (sm_100a) constant-pH lambda-dynamics step library.
+ *
+ * What one step computes (arXiv 2410.01626 as read in DESIGN.md):
+ *   a1  lambda -> charges, q_i = sum_s w_s(lp, lt) q_i^s with the Eq. 2 weights
+ *       (PAPER.md:618-632); only charges differ between forms;
+ *       charge-buffer oxygens switch -0.834 -> +0.166 e.
+ *   a2  cell-list Verlet pair list, rebuilt every nstlist steps.
+ *   a3  real-space Ewald + Lennard-Jones pair kernel accumulating forces and the
+ *       per-atom potential phi_i.
+ *   a4-a7  smooth PME: B-spline spread, 3D FFT (cuFFT), influence-function
+ *       solve, potential/force gather.
+ *   a8  dV/dlambda_k = f sum_{i in k} (dq_i/dlambda_k) phi_i reduced in fp64 per
+ *       lambda-group, plus the bias V = Vmm + VpH + Vdw (Eq. 3, PAPER.md:667-698,
+ *       :715-740).
+ *   a9  BAOAB Langevin / velocity-Verlet update of atoms and lambda particles
+ *       (m_lambda = 60 u), dt = 2 fs, 300 K.
+ *   a10 Partition Function Correction of the double-well depths at cph_create /
+ *       cph_set_pH.
+ *
+ * Conventions
+ *   Units: nm, ps, u, kJ/mol, e, K.  lambda = 0 is protonated; a frame is
+ *   deprotonated iff lambda_p >= 0.5 (reading R1).
+ *   Coordinates: group g of kind 2 owns one coordinate (lp); kind 3 (His-like)
+ *   owns two (lp, lt).  The flat lambda vector of a replica concatenates them
+ *   in group order; C = number of coordinates.
+ *   Atom order: every getter returns ORIGINAL atom order (the order of
+ *   cph_system.pos), whatever order the device keeps internally.
+ *   Replicas: one context batches R replicas of the same system (same
+ *   topology and box), which differ in pH, seed, initial lambda, positions and
+ *   velocities.  Every kernel launch covers all R replicas.
+ *
+ * Ownership: input pointers are borrowed for the duration of the call and
+ *   copied.  Output buffers are caller-owned host memory.  Device memory is
+ *   owned by the context; it is obtained through params.dev_alloc/dev_free when
+ *   given (the Python binding passes PyTorch's caching allocator) or cudaMalloc.
+ * Errors: every call returns a cph_status; nothing throws across the ABI.
+ *   cph_last_error(ctx) gives a message (ctx == NULL: last cph_create failure
+ *   of this thread).  cph_step is asynchronous on params.cuda_stream; device
+ *   side failures (lambda divergence |lambda| > 10 or non-finite dV/dlambda,
+ *   pair-list overflow) are latched and reported by the next call.
+ * Threading: a context is not thread-safe; use one per host thread.
+ */
+#ifndef CPH_H
+#define CPH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CPH_ABI_VERSION 1
+
+typedef struct cph_ctx cph_ctx;
+
+typedef enum {
+  CPH_OK = 0,
+  CPH_E_INVALID = 1,     /* invalid argument or inconsistent system */
+  CPH_E_CUDA = 2,        /* CUDA / cuFFT runtime error */
+  CPH_E_DIVERGED = 3,    /* |lambda| > 10 or non-finite dV/dlambda */
+  CPH_E_STATE = 4,       /* call not valid in the current state (e.g. list overflow, rebuilt) */
+  CPH_E_OOM = 5,         /* device allocation failed */
+  CPH_E_UNSUPPORTED = 6  /* valid request outside what this build implements */
+} cph_status;
+
+/* energy terms returned by cph_get_energies, kJ/mol */
+enum {
+  CPH_E_LJ = 0, CPH_E_REAL, CPH_E_EXCL, CPH_E_SELF, CPH_E_RECIP, CPH_E_NET,
+  CPH_E_BIAS, CPH_E_KE_ATOMS, CPH_E_KE_LAMBDA, CPH_E_TOTAL, CPH_N_ETERMS
+};
+
+/* kernel classes timed by cph_profile_steps */
+enum {
+  CPH_K_INTEGRATE = 0, CPH_K_PAIRLIST, CPH_K_NONBONDED, CPH_K_SPREAD, CPH_K_FFT_R2C,
+  CPH_K_SOLVE, CPH_K_FFT_C2R, CPH_K_GATHER, CPH_K_LAMBDA, CPH_N_KCLASSES
+};
+
+typedef struct {
+  int32_t n_atoms;              /* N >= 1, N < 2^24 */
+  const float *pos;             /* [N*3] nm, any image */
+  const float *vel;             /* [N*3] nm/ps or NULL (zero) */
+  const float *mass;            /* [N] u; 0 = frozen (never moved) */
+  const float *charge;          /* [N] e; used for atoms that are in no lambda-group */
+  const int32_t *type;          /* [N] LJ type in [0, n_types) */
+  int32_t n_types;              /* 1..255 */
+  const double *c6;             /* [T*T] kJ mol^-1 nm^6, symmetric */
+  const double *c12;            /* [T*T] kJ mol^-1 nm^12, symmetric */
+  int32_t n_excl;               /* number of excluded pairs */
+  const int32_t *excl;          /* [2*n_excl] unordered atom pairs, i != j */
+  double box[3];                /* rectangular box edges, nm */
+  int32_t n_groups;             /* G >= 0 lambda-groups */
+  const int32_t *group_kind;    /* [G] 2 (one coordinate) or 3 (two coordinates) */
+  const int32_t *group_ptr;     /* [G+1] CSR offsets into group_atoms */
+  const int32_t *group_atoms;   /* [n_group_atoms] atom indices, each atom in <= 1 group */
+  const double *state_q;        /* [n_group_atoms*4] charges of forms A,B,C,D (Eq. 2);
+                                   kind 2 requires A == B and C == D */
+  const int32_t *is_buffer;     /* [n_group_atoms] 1 for the charge-buffer member, or NULL */
+  const double *pKa;            /* [G*3] macro, micro-delta, micro-eps (kind 2 uses macro) */
+  const double *vmm;            /* [G*36] Vmm coefficients c[a*6+b] of lp^a lt^b */
+} cph_system;
+
+typedef struct {
+  int32_t abi_version;          /* = CPH_ABI_VERSION */
+  int32_t n_replicas;           /* R >= 1 */
+  int32_t device;               /* CUDA device ordinal */
+  int32_t mode;                 /* 0 lambda dynamics; 1 fixed-lambda TI (lambda frozen,
+                                   dV/dlambda accumulated for cph_get_ti_means) */
+  double dt;                    /* ps (0.002) */
+  double temperature;           /* K (300) */
+  double gamma_atom;            /* ps^-1 Langevin friction of atoms (1) */
+  double gamma_lambda;          /* ps^-1 friction of lambda particles (1 = 1/tau) */
+  double lambda_mass;           /* u (60) */
+  double rc;                    /* nm real-space / LJ cut-off (1.0) */
+  double rlist;                 /* nm pair-list radius (1.1), rc <= rlist < min(box)/2 */
+  double ewald_rtol;            /* erfc(beta rc) = ewald_rtol (1e-5) */
+  int32_t pme_grid[3];          /* K_x, K_y, K_z: even, factors 2,3,5,7 only */
+  int32_t pme_order;            /* 4 (only order supported) */
+  int32_t nstlist;              /* pair-list rebuild interval (10) */
+  int32_t nstout;               /* lambda frame interval (250 = 0.5 ps) */
+  int32_t nstenergy;            /* energy evaluation interval (250) */
+  double barrier;               /* kJ/mol double-well barrier h (6) */
+  double wall_k;                /* kJ/mol quartic wall constant (1e6) */
+  const double *pH;             /* [R] */
+  const uint64_t *replica_seed; /* [R] Philox keys */
+  const double *lambda0;        /* [R*C] initial lambda or NULL (all 0 = protonated) */
+  const float *pos_replicas;    /* [R*N*3] per-replica positions or NULL (system pos) */
+  const float *vel_replicas;    /* [R*N*3] per-replica velocities or NULL (system vel) */
+  int32_t frame_capacity;       /* lambda frames kept per replica between cph_get_frames (>=1) */
+  void *cuda_stream;            /* cudaStream_t to launch on (NULL = legacy default) */
+  void *(*dev_alloc)(size_t bytes, void *alloc_ctx);   /* NULL -> cudaMalloc */
+  void (*dev_free)(void *ptr, void *alloc_ctx);
+  void *alloc_ctx;
+} cph_params;
+
+/* Fill *p with the defaults quoted above (pH/seed pointers NULL). */
+void cph_default_params(cph_params *p);
+
+/* Validate, copy to the device, run the PFC for every replica's pH, build the
+ * pair list and evaluate forces/potentials/energies at step 0.
+ * CPH_E_INVALID: non-finite input, bad sizes, a group whose total charge
+ * varies with lambda, rlist >= min(box)/2, rc > rlist.
+ * CPH_E_UNSUPPORTED: pme_order != 4, grid not even / not 2,3,5,7-smooth. */
+cph_status cph_create(const cph_system *sys, const cph_params *params, cph_ctx **out);
+void cph_destroy(cph_ctx *ctx);
+
+/* Number of lambda coordinates C per replica and atoms N. */
+int32_t cph_n_coords(const cph_ctx *ctx);
+int32_t cph_n_atoms(const cph_ctx *ctx);
+int32_t cph_n_replicas(const cph_ctx *ctx);
+
+/* Change one replica's pH: recomputes the PFC well depths (host) and uploads
+ * them; takes effect at the next step.  replica in [0, R). */
+cph_status cph_set_pH(cph_ctx *ctx, int32_t replica, double pH);
+
+/* Advance all replicas by n_steps >= 0 (asynchronous on the context stream). */
+cph_status cph_step(cph_ctx *ctx, int64_t n_steps);
+
+/* Block until the context stream is idle; reports latched device errors. */
+cph_status cph_sync(cph_ctx *ctx);
+
+/* Current step index (number of completed steps since create). */
+int64_t cph_current_step(const cph_ctx *ctx);
+
+/* Getters (synchronize first).  replica in [0, R). */
+cph_status cph_get_lambdas(cph_ctx *ctx, int32_t replica, double *lam /*[C]*/, double *vel /*[C] or NULL*/);
+/* dV/dlambda at the current state: Coulomb part f sum dq/dl phi, and bias part. */
+cph_status cph_get_dvdl(cph_ctx *ctx, int32_t replica, double *coul /*[C]*/, double *bias /*[C]*/);
+/* Energies at the current state in the CPH_E_* order; total = sum of the others. */
+cph_status cph_get_energies(cph_ctx *ctx, int32_t replica, double *e /*[CPH_N_ETERMS]*/);
+/* PFC results: lambda=1 well depth d1 per coordinate (kJ/mol). */
+cph_status cph_get_bias_params(cph_ctx *ctx, int32_t replica, double *d1 /*[C]*/);
+/* lambda frames recorded every nstout steps since the last call (oldest first);
+ * buf [cap*C] floats; *n_frames = frames written; frames beyond capacity are
+ * dropped oldest-first and *n_dropped reports how many. */
+cph_status cph_get_frames(cph_ctx *ctx, int32_t replica, float *buf, int64_t cap,
+                          int64_t *n_frames, int64_t *n_dropped);
+/* Force on every atom [3N] (kJ mol^-1 nm^-1) and the full electrostatic potential
+ * phi_i = (1/f) dE_coul/dq_i [N] (e/nm; real + exclusion + reciprocal + self +
+ * net-charge terms), original order.  Either pointer may be NULL. */
+cph_status cph_get_forces(cph_ctx *ctx, int32_t replica, float *f, float *phi);
+/* Current positions [3N] and velocities [3N] (original order); either may be NULL. */
+cph_status cph_get_positions(cph_ctx *ctx, int32_t replica, float *pos, float *vel);
+/* Canonical pair list of the last rebuild: non-excluded pairs (i<j, original
+ * indices) with float32 d^2 < rlist^2, lexicographically sorted, as [2*n].
+ * If cap < n nothing is written and *n tells the size needed. */
+cph_status cph_get_pairlist(cph_ctx *ctx, int32_t replica, int32_t *pairs, int64_t cap, int64_t *n);
+/* Mean dV/dlambda (coul+bias) per coordinate over the steps since create or the
+ * last call (mode 1, TI), and the number of samples. */
+cph_status cph_get_ti_means(cph_ctx *ctx, int32_t replica, double *mean /*[C]*/, int64_t *n_samples);
+/* Checkpoint of one replica: size query with buf == NULL (*n gets bytes). */
+cph_status cph_get_state(cph_ctx *ctx, int32_t replica, void *buf, int64_t cap, int64_t *n);
+cph_status cph_set_state(cph_ctx *ctx, int32_t replica, const void *buf, int64_t n);
+
+/* Run n_steps eagerly with CUDA events around every kernel class (serialised,
+ * one stream) and return the summed milliseconds per class [CPH_N_KCLASSES]
+ * and the number of launches per class [CPH_N_KCLASSES] (either may be NULL). */
+cph_status cph_profile_steps(cph_ctx *ctx, int64_t n_steps, double *ms, int64_t *launches);
+/* Number of kernel launches of this library issued so far (graph replays
+ * counted per contained kernel; cuFFT's internal kernels not included). */
+int64_t cph_launch_count(const cph_ctx *ctx);
+
+const char *cph_last_error(const cph_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPH_H */

@@ -1,0 +1,146 @@
+// Device helpers shared by the library's kernels (not by the oracle).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cph_internal.cuh"
+
+namespace cph {
+
+// ---------------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11).  key = (seed lo, seed hi); counters per
+// DESIGN.md R17: atoms (step, atom, 0, 0), lambda (step, coord, 1, 0).
+// ---------------------------------------------------------------------------------
+struct U4 { uint32_t x, y, z, w; };
+
+__host__ __device__ inline U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+#ifdef __CUDA_ARCH__
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+#else
+    uint64_t p0 = (uint64_t)0xD2511F53u * c.x, p1 = (uint64_t)0xCD9E8D57u * c.z;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+#endif
+    U4 n;
+    n.x = hi1 ^ c.y ^ k0; n.y = lo1; n.z = hi0 ^ c.w ^ k1; n.w = lo0;
+    c = n;
+  }
+  return c;
+}
+
+// three fp32 standard normals for an atom (Box-Muller on u = (x + 0.5) 2^-32)
+__device__ inline float3 atom_normals(uint64_t seed, uint32_t step, uint32_t atom) {
+  U4 o = philox4x32_10(U4{step, atom, 0u, 0u}, (uint32_t)seed, (uint32_t)(seed >> 32));
+  const float s = 2.3283064365386963e-10f;  // 2^-32
+  float u0 = ((float)o.x + 0.5f) * s, u1 = ((float)o.y + 0.5f) * s;
+  float u2 = ((float)o.z + 0.5f) * s, u3 = ((float)o.w + 0.5f) * s;
+  // u0 may round to 1.0f in fp32: log(1) = 0 gives a zero radius, harmless
+  float r0 = sqrtf(-2.0f * logf(u0)), r1 = sqrtf(-2.0f * logf(u2));
+  float s0, c0, s1, c1;
+  sincospif(2.0f * u1, &s0, &c0);
+  sincospif(2.0f * u3, &s1, &c1);
+  return make_float3(r0 * c0, r0 * s0, r1 * c1);
+}
+
+// one fp64 standard normal for a lambda coordinate
+__device__ inline double lambda_normal(uint64_t seed, uint32_t step, uint32_t coord) {
+  U4 o = philox4x32_10(U4{step, coord, 1u, 0u}, (uint32_t)seed, (uint32_t)(seed >> 32));
+  double u0 = ((double)o.x + 0.5) * 2.3283064365386963e-10;
+  double u1 = ((double)o.y + 0.5) * 2.3283064365386963e-10;
+  return sqrt(-2.0 * log(u0)) * cospi(2.0 * u1);
+}
+
+// ---------------------------------------------------------------------------------
+// erfc(z) = t P(t) exp(-z^2), t = 1/(1 + p z): least-squares-minimax fit of
+// erfcx(z)/t on z in [0, 4] (rel. error 3e-8 in exact arithmetic, 4e-7 in fp32).
+// exp(-z^2) is shared with the Ewald force term.
+// ---------------------------------------------------------------------------------
+constexpr float kErfcP = 0.3275911f;
+__device__ __forceinline__ float erfc_poly(float t) {
+  float a = -1.348251700e-01f;
+  a = fmaf(a, t, 4.629509449e-01f);
+  a = fmaf(a, t, -3.302423954e-01f);
+  a = fmaf(a, t, 3.610785306e-01f);
+  a = fmaf(a, t, 9.128254652e-02f);
+  a = fmaf(a, t, 1.782859266e-01f);
+  a = fmaf(a, t, 1.870171428e-01f);
+  a = fmaf(a, t, 1.844524294e-01f);
+  return a * t;   // erfc(z) * exp(z^2)
+}
+
+// minimum image with the canonical fp32 formula (round-to-nearest, no contraction)
+__device__ __forceinline__ float min_image_rn(float dx, float L, float invL) {
+  return __fsub_rn(dx, __fmul_rn(L, rintf(__fmul_rn(dx, invL))));
+}
+
+// ---------------------------------------------------------------------------------
+// Bias potential pieces (host + device, fp64).  DESIGN.md R4/R5:
+//   Vdw: cubic Hermite through (0,0,0), (0.5,h,0), (1,d1,0), mirrored outside
+//   [0,1], quartic walls k_w (l+0.1)^4 below -0.1 and k_w (l-1.1)^4 above 1.1.
+// ---------------------------------------------------------------------------------
+__host__ __device__ inline void vdw_eval(double lam, double h, double d1, double kw, double *v,
+                                         double *dv) {
+  double x = lam, sgn = 1.0;
+  if (lam < 0.0) { x = -lam; sgn = -1.0; }
+  else if (lam > 1.0) { x = 2.0 - lam; sgn = -1.0; }
+  x = x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x);
+  double a, b, t;
+  if (x <= 0.5) { a = 0.0; b = h; t = 2.0 * x; }
+  else { a = h; b = d1; t = 2.0 * (x - 0.5); }
+  double val = a + (b - a) * t * t * (3.0 - 2.0 * t);
+  double der = sgn * 2.0 * (b - a) * 6.0 * t * (1.0 - t);
+  if (lam < -0.1) { double w = lam + 0.1; val += kw * w * w * w * w; der += 4.0 * kw * w * w * w; }
+  else if (lam > 1.1) { double w = lam - 1.1; val += kw * w * w * w * w; der += 4.0 * kw * w * w * w; }
+  *v = val;
+  *dv = der;
+}
+
+__host__ __device__ inline void vmm_eval(const double *c, double lp, double lt, double *v, double *dp,
+                                         double *dt) {
+  double pp[6], pt[6];
+  pp[0] = pt[0] = 1.0;
+  for (int k = 1; k < 6; ++k) { pp[k] = pp[k - 1] * lp; pt[k] = pt[k - 1] * lt; }
+  double V = 0, DP = 0, DT = 0;
+  for (int a = 0; a < 6; ++a)
+    for (int b = 0; b < 6; ++b) {
+      double cab = c[a * 6 + b];
+      V += cab * pp[a] * pt[b];
+      if (a) DP += a * cab * pp[a - 1] * pt[b];
+      if (b) DT += b * cab * pp[a] * pt[b - 1];
+    }
+  *v = V; *dp = DP; *dt = DT;
+}
+
+__device__ inline double warp_sum_d(double v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ inline float warp_sum_f(float v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block-reduce a double into one atomicAdd (blockDim multiple of 32, <= 1024)
+__device__ inline void block_atomic_add_d(double v, double *dst) {
+  __shared__ double red[32];
+  v = warp_sum_d(v);
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int nw = (blockDim.x + 31) >> 5;
+    double s = lane < nw ? red[lane] : 0.0;
+    s = warp_sum_d(s);
+    if (lane == 0 && s != 0.0) atomicAdd(dst, s);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool is_energy_step(long long m, long long end, int nstenergy) {
+  return (m % nstenergy) == 0 || m == end;
+}
+
+}  // namespace cph

@@ -1,0 +1,146 @@
+// Internal declarations of the cph library (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/cph.h"
+
+namespace cph {
+
+// ---- physical constants (own copy; the oracle keeps its own) -----------------------
+constexpr double kFCoul = 138.935458;        // kJ mol^-1 nm e^-2
+constexpr double kBoltz = 0.0083144626;      // kJ mol^-1 K^-1
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kLn10 = 2.30258509299404568402;
+
+constexpr int kNE = CPH_N_ETERMS;
+constexpr int kMaxTypes = 32;                // LJ table kept in shared memory
+
+// Device-side flags (int array)
+enum { FLAG_PENDING_CLOSE = 0, FLAG_LIST_OVERFLOW = 1, FLAG_DIVERGED = 2, FLAG_MAX_NNB = 3,
+       FLAG_STEP_DONE = 4, FLAG_COUNT = 8 };
+
+// Scalars every kernel needs, passed by value.
+struct KParams {
+  int R, N, Nst;               // replicas, atoms, per-replica stride (multiple of 32)
+  float L[3], invL[3];         // box (fp32) and 1/L (fp32, computed as 1.0f/L)
+  double Ld[3];
+  float rc2, rlist2;
+  float beta, beta_p;          // Ewald beta, beta * p (erfc polynomial scale)
+  float two_beta_sqrtpi;       // 2 beta / sqrt(pi)
+  float fcoul;
+  int T;                       // LJ types
+  // cells
+  int nc[3], ncell;            // cells per dimension, total
+  int ns[3], so[3];            // stencil sizes and first offsets per dimension
+  // list
+  int cap;                     // neighbour capacity per atom
+  // PME
+  int K[3], K3, Kc;            // grid, K^3, complex points per replica
+  int Kzc;                     // Kz/2+1
+  float V;                     // volume nm^3
+  // dynamics
+  float dt, kT_f;
+  double dtd, kT;
+  float c1_atom, c2_atom_kT;   // exp(-g dt), (1-c1^2) kT
+  double c1_lam, sd_lam;       // exp(-g_l dt), sqrt((1-c1^2) kT / m_l)
+  double m_lam;
+  int nstout, nstenergy, nstlist;
+  int mode;
+  // lambda groups
+  int G, C, nlam;
+  double beta_d;
+  double Q_fixed, Q2_fixed;    // sum and sum of squares of fixed charges (per replica identical)
+  double h_barrier, wall_k;
+  int fcap;                    // frame capacity
+};
+
+struct DevBufs {
+  float4 *xyzq = nullptr, *xyzq_alt = nullptr;
+  float4 *vel = nullptr, *vel_alt = nullptr;
+  int2 *meta = nullptr, *meta_alt = nullptr;       // (orig, type | (lslot+1) << 8)
+  float4 *f_nb = nullptr, *f_rec = nullptr;
+  int *iperm = nullptr;                             // [R*N] orig -> slot
+  int *cell_of = nullptr, *cell_rank = nullptr;     // [R*Nst]
+  int *cell_count = nullptr, *cell_start = nullptr; // [R*ncell], [R*(ncell+1)]
+  int *perm_tmp = nullptr;                          // [R*Nst] new slot -> old slot
+  uint32_t *nbl = nullptr;                          // [R*cap*Nst]
+  int *nnb = nullptr;                               // [R*Nst]
+  int *excl_ptr = nullptr, *excl_idx = nullptr;     // CSR by original atom
+  float2 *ljtab = nullptr;                          // [T*T] (6 c6, 12 c12) fp32
+  double *phi64_nb = nullptr, *phi64_rec = nullptr; // [R*nlam]
+  float *grid = nullptr;                            // [R*K3]
+  float2 *cgrid = nullptr;                          // [R*Kc]
+  float *bsp = nullptr;                             // [Kx + Ky + Kz] |b|^2 moduli
+  int *g_kind = nullptr, *g_ptr = nullptr, *g_atoms = nullptr, *g_cptr = nullptr;
+  double *g_q = nullptr;                            // [nlam*4]
+  double *vmm = nullptr;                            // [G*36]
+  double *g_dG = nullptr;                           // [R*G*3] dG macro, delta, eps at pH
+  double *d1 = nullptr;                             // [R*C]
+  double *lam = nullptr, *lamv = nullptr;           // [R*C]
+  double *qlam = nullptr;                           // [R*nlam]
+  double *dvdl_coul = nullptr, *dvdl_bias = nullptr;// [R*C]
+  double *ti_sum = nullptr;                         // [R*C]
+  long long *ti_n = nullptr;                        // [1]
+  double *erec = nullptr;                           // [2*R*kNE]
+  float *frames = nullptr;                          // [R*fcap*C]
+  long long *frame_total = nullptr;                 // [R]
+  long long *step = nullptr, *end_step = nullptr;   // device step counter, last step of call
+  int *done_counter = nullptr;
+  int *flags = nullptr;
+  uint64_t *seed = nullptr;                         // [R]
+  double *phi_lam = nullptr;                        // [R*nlam] total phi of lambda atoms
+};
+
+struct Ctx {
+  KParams kp{};
+  DevBufs d;
+  cudaStream_t stream = nullptr, stream_pme = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool own_stream = false;
+  cufftHandle plan_r2c = 0, plan_c2r = 0;
+  void *(*dev_alloc)(size_t, void *) = nullptr;
+  void (*dev_free)(void *, void *) = nullptr;
+  void *alloc_ctx = nullptr;
+  std::vector<void *> allocations;
+  int device = 0;
+  // host copies
+  std::vector<int> h_group_kind, h_group_ptr, h_group_atoms, h_cptr;
+  std::vector<double> h_state_q, h_pKa, h_pH;
+  std::vector<int> h_excl_ptr, h_excl_idx;
+  std::vector<uint64_t> h_seed;
+  std::vector<double> h_d1;                         // [R*C]
+  int *h_flags_mapped = nullptr;                    // host view of a mapped flag copy
+  int *d_flags_mapped = nullptr;
+  long long host_step = 0;
+  int64_t launches = 0;
+  // CUDA graph of one nstlist block (rebuild at first step)
+  cudaGraphExec_t graph_block = nullptr;
+  int graph_block_kernels = 0;
+  std::string err;
+  size_t cap_grow = 0;
+};
+
+// ---- launchers (each returns the number of kernels it launched) ----------------------
+int launch_integrate(Ctx &c, cudaStream_t s, int do_open);       // BAOA (+ pending close)
+int launch_close(Ctx &c, cudaStream_t s, int kick);                // final half kick / KE
+int launch_rebuild(Ctx &c, cudaStream_t s);                        // sort + pair list
+int launch_nonbonded(Ctx &c, cudaStream_t s, int step_offset);
+int launch_spread(Ctx &c, cudaStream_t s);
+int launch_solve(Ctx &c, cudaStream_t s, int step_offset);
+int launch_gather(Ctx &c, cudaStream_t s);
+int launch_lambda_reduce(Ctx &c, cudaStream_t s, int mode);       // 0 init eval, 1 step
+int launch_lambda_open(Ctx &c, cudaStream_t s);
+int launch_set_charges(Ctx &c, cudaStream_t s);
+
+// host PFC (pfc.cpp)
+bool pfc_two_state(double h, double pKa, double pH, double T, double kw, double *d1, std::string *err);
+bool pfc_three_state(double h, const double pKa3[3], double pH, double T, double kw, double *d1p,
+                     double *d1t, std::string *err);
+double delta_g(double pKa, double pH, double T);
+
+}  // namespace cph

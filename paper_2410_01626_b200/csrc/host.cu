@@ -1,0 +1,927 @@
+// Host runtime behind include/cph.h: validation, device memory, PFC, cuFFT plans, step
+// scheduling (CUDA graph per nstlist block, nonbonded || PME on two streams), getters.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "cph_device.cuh"
+
+using namespace cph;
+
+struct cph_ctx {
+  Ctx c;
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+#define CK(call)                                                                  \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess) {                                                      \
+      c.err = std::string(#call) + ": " + cudaGetErrorString(e_);                 \
+      return CPH_E_CUDA;                                                          \
+    }                                                                             \
+  } while (0)
+
+#define CKF(call)                                                                 \
+  do {                                                                            \
+    cufftResult r_ = (call);                                                      \
+    if (r_ != CUFFT_SUCCESS) {                                                    \
+      c.err = std::string(#call) + ": cuFFT error " + std::to_string((int)r_);    \
+      return CPH_E_CUDA;                                                          \
+    }                                                                             \
+  } while (0)
+
+template <class T>
+T *dalloc(Ctx &c, size_t count) {
+  size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  void *p = nullptr;
+  if (c.dev_alloc) p = c.dev_alloc(bytes, c.alloc_ctx);
+  else if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
+  if (p) {
+    c.allocations.push_back(p);
+    cudaMemset(p, 0, bytes);
+  }
+  return (T *)p;
+}
+
+void free_all(Ctx &c) {
+  for (void *p : c.allocations) {
+    if (c.dev_free) c.dev_free(p, c.alloc_ctx);
+    else cudaFree(p);
+  }
+  c.allocations.clear();
+}
+
+bool smooth2357(int k) {
+  if (k <= 0) return false;
+  for (int f : {2, 3, 5, 7})
+    while (k % f == 0) k /= f;
+  return k == 1;
+}
+
+double erfc_beta(double rc, double rtol) {
+  double lo = 0.0, hi = 50.0 / rc;
+  for (int i = 0; i < 200; ++i) {
+    const double mid = 0.5 * (lo + hi);
+    if (std::erfc(mid * rc) > rtol) lo = mid; else hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+double bspline4_at(double t) {   // M4 at integer arguments 1, 2, 3
+  if (t == 1.0 || t == 3.0) return 1.0 / 6.0;
+  if (t == 2.0) return 4.0 / 6.0;
+  return 0.0;
+}
+
+void bsp_moduli(int K, std::vector<float> &out) {
+  for (int m = 0; m < K; ++m) {
+    double re = 0.0, im = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const double a = 2.0 * kPi * m * k / K;
+      re += bspline4_at(k + 1.0) * std::cos(a);
+      im += bspline4_at(k + 1.0) * std::sin(a);
+    }
+    out.push_back((float)(1.0 / (re * re + im * im)));
+  }
+}
+
+bool finite_arr(const float *p, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+bool finite_arr(const double *p, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+cph_status run_pfc(Ctx &c, int r) {
+  const KParams &kp = c.kp;
+  const double pH = c.h_pH[r];
+  std::vector<double> dG((size_t)kp.G * 3), d1((size_t)kp.C);
+  for (int g = 0; g < kp.G; ++g) {
+    const double *pk = &c.h_pKa[(size_t)g * 3];
+    for (int k = 0; k < 3; ++k) dG[(size_t)g * 3 + k] = delta_g(pk[k], pH, kp.kT / kBoltz);
+    const int c0 = c.h_cptr[g];
+    std::string err;
+    if (c.h_group_kind[g] == 2) {
+      if (!pfc_two_state(kp.h_barrier, pk[0], pH, kp.kT / kBoltz, kp.wall_k, &d1[c0], &err)) {
+        c.err = err;
+        return CPH_E_INVALID;
+      }
+    } else {
+      if (!pfc_three_state(kp.h_barrier, pk, pH, kp.kT / kBoltz, kp.wall_k, &d1[c0], &d1[c0 + 1], &err)) {
+        c.err = err;
+        return CPH_E_INVALID;
+      }
+    }
+  }
+  std::copy(d1.begin(), d1.end(), c.h_d1.begin() + (size_t)r * kp.C);
+  if (kp.C) CK(cudaMemcpy(c.d.d1 + (size_t)r * kp.C, d1.data(), sizeof(double) * kp.C, cudaMemcpyHostToDevice));
+  if (kp.G) CK(cudaMemcpy(c.d.g_dG + (size_t)r * kp.G * 3, dG.data(), sizeof(double) * kp.G * 3, cudaMemcpyHostToDevice));
+  return CPH_OK;
+}
+
+__global__ void k_set_end(long long *end, long long v) { *end = v; }
+
+// one full step (n -> n+1) on the context streams; returns kernels launched
+int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
+  int k = 0;
+  cudaStream_t s = c.stream;
+  k += launch_integrate(c, s, 1);
+  if (rebuild) k += launch_rebuild(c, s);
+  cudaStream_t sp = s;
+  if (two_streams) {
+    cudaEventRecord(c.ev_fork, s);
+    cudaStreamWaitEvent(c.stream_pme, c.ev_fork, 0);
+    sp = c.stream_pme;
+  }
+  cufftSetStream(c.plan_r2c, sp);
+  cufftSetStream(c.plan_c2r, sp);
+  k += launch_spread(c, sp);
+  cufftExecR2C(c.plan_r2c, c.d.grid, (cufftComplex *)c.d.cgrid);
+  k += launch_solve(c, sp, 1);
+  cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid);
+  k += launch_gather(c, sp);
+  k += launch_nonbonded(c, s, 1);
+  if (two_streams) {
+    cudaEventRecord(c.ev_join, c.stream_pme);
+    cudaStreamWaitEvent(s, c.ev_join, 0);
+  }
+  k += launch_lambda_reduce(c, s, 1);
+  return k;
+}
+
+// evaluation at the current state without integration (create / set_state)
+cph_status evaluate_here(Ctx &c) {
+  cudaStream_t s = c.stream;
+  k_set_end<<<1, 1, 0, s>>>(c.d.end_step, c.host_step);
+  CK(cudaMemsetAsync(c.d.erec + (size_t)(c.host_step & 1) * c.kp.R * kNE, 0, sizeof(double) * c.kp.R * kNE, s));
+  int k = 1;
+  k += launch_set_charges(c, s);
+  k += launch_rebuild(c, s);
+  cufftSetStream(c.plan_r2c, s);
+  cufftSetStream(c.plan_c2r, s);
+  k += launch_spread(c, s);
+  CKF(cufftExecR2C(c.plan_r2c, c.d.grid, (cufftComplex *)c.d.cgrid));
+  k += launch_solve(c, s, 0);
+  CKF(cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid));
+  k += launch_gather(c, s);
+  k += launch_nonbonded(c, s, 0);
+  k += launch_lambda_reduce(c, s, 0);
+  k += launch_close(c, s, 0);
+  c.launches += k;
+  CK(cudaGetLastError());
+  return CPH_OK;
+}
+
+cph_status check_flags(Ctx &c) {
+  int f[FLAG_COUNT];
+  CK(cudaStreamSynchronize(c.stream));
+  CK(cudaMemcpy(f, c.d.flags, sizeof(f), cudaMemcpyDeviceToHost));
+  if (f[FLAG_DIVERGED]) {
+    c.err = "lambda diverged (|lambda| > 10 or non-finite dV/dlambda)";
+    return CPH_E_DIVERGED;
+  }
+  if (f[FLAG_LIST_OVERFLOW]) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "pair list overflow: %d neighbours > capacity %d; results since the last rebuild are invalid",
+             f[FLAG_MAX_NNB], c.kp.cap);
+    c.err = buf;
+    c.cap_grow = (size_t)f[FLAG_MAX_NNB];
+    return CPH_E_STATE;
+  }
+  return CPH_OK;
+}
+
+cph_status capture_block(Ctx &c) {
+  if (c.graph_block) return CPH_OK;
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  int k = 0;
+  for (int s = 0; s < c.kp.nstlist; ++s) k += enqueue_step(c, s == c.kp.nstlist - 1, true);
+  CK(cudaStreamEndCapture(c.stream, &g));
+  CK(cudaGraphInstantiate(&c.graph_block, g, 0));
+  cudaGraphDestroy(g);
+  c.graph_block_kernels = k;
+  return CPH_OK;
+}
+
+cph_status check_replica(Ctx &c, int r) {
+  if (r < 0 || r >= c.kp.R) {
+    c.err = "replica index out of range";
+    return CPH_E_INVALID;
+  }
+  return CPH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void cph_default_params(cph_params *p) {
+  std::memset(p, 0, sizeof(*p));
+  p->abi_version = CPH_ABI_VERSION;
+  p->n_replicas = 1;
+  p->dt = 0.002;
+  p->temperature = 300.0;
+  p->gamma_atom = 1.0;
+  p->gamma_lambda = 1.0;
+  p->lambda_mass = 60.0;
+  p->rc = 1.0;
+  p->rlist = 1.1;
+  p->ewald_rtol = 1e-5;
+  p->pme_grid[0] = p->pme_grid[1] = p->pme_grid[2] = 32;
+  p->pme_order = 4;
+  p->nstlist = 10;
+  p->nstout = 250;
+  p->nstenergy = 250;
+  p->barrier = 6.0;
+  p->wall_k = 1e6;
+  p->frame_capacity = 1024;
+}
+
+const char *cph_last_error(const cph_ctx *ctx) { return ctx ? ctx->c.err.c_str() : g_create_err.c_str(); }
+
+static cph_status fail_create(cph_ctx *ctx, cph_status st) {
+  g_create_err = ctx->c.err;
+  free_all(ctx->c);
+  delete ctx;
+  return st;
+}
+
+cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **out) {
+  if (!out) { g_create_err = "out is NULL"; return CPH_E_INVALID; }
+  *out = nullptr;
+  if (!sys || !prm) { g_create_err = "system/params is NULL"; return CPH_E_INVALID; }
+  cph_ctx *ctx = new cph_ctx;
+  Ctx &c = ctx->c;
+  auto bad = [&](const char *m) { c.err = m; return fail_create(ctx, CPH_E_INVALID); };
+  if (prm->abi_version != CPH_ABI_VERSION) return bad("abi_version mismatch");
+  const int N = sys->n_atoms, R = prm->n_replicas, G = sys->n_groups, T = sys->n_types;
+  if (N < 1 || N >= (1 << 24)) return bad("n_atoms must be in [1, 2^24)");
+  if (R < 1) return bad("n_replicas must be >= 1");
+  if (!sys->pos || !sys->mass || !sys->charge || !sys->type || !sys->c6 || !sys->c12)
+    return bad("system arrays pos/mass/charge/type/c6/c12 are required");
+  if (T < 1 || T > kMaxTypes) return bad("n_types must be in [1, 32]");
+  if (!finite_arr(sys->pos, 3 * (size_t)N) || !finite_arr(sys->mass, N) || !finite_arr(sys->charge, N) ||
+      (sys->vel && !finite_arr(sys->vel, 3 * (size_t)N)) || !finite_arr(sys->c6, (size_t)T * T) ||
+      !finite_arr(sys->c12, (size_t)T * T) || !finite_arr(sys->box, 3))
+    return bad("non-finite value in system");
+  for (int i = 0; i < N; ++i) {
+    if (sys->mass[i] < 0.0f) return bad("negative mass");
+    if (sys->type[i] < 0 || sys->type[i] >= T) return bad("type out of range");
+  }
+  for (int d = 0; d < 3; ++d)
+    if (!(sys->box[d] > 0.0)) return bad("box edges must be > 0");
+  if (!(prm->rc > 0.0) || !(prm->rlist >= prm->rc)) return bad("need 0 < rc <= rlist");
+  for (int d = 0; d < 3; ++d)
+    if (!(prm->rlist < 0.5 * sys->box[d])) return bad("rlist must be < half of every box edge");
+  if (!(prm->dt > 0.0) || !(prm->temperature > 0.0) || !(prm->lambda_mass > 0.0) || prm->gamma_atom < 0.0 ||
+      prm->gamma_lambda < 0.0 || !(prm->ewald_rtol > 0.0 && prm->ewald_rtol < 1.0))
+    return bad("invalid dynamics / Ewald parameter");
+  if (prm->nstlist < 1 || prm->nstout < 1 || prm->nstenergy < 1 || prm->frame_capacity < 1)
+    return bad("nstlist, nstout, nstenergy, frame_capacity must be >= 1");
+  if (prm->mode != 0 && prm->mode != 1) return bad("mode must be 0 or 1");
+  if (!prm->pH || !prm->replica_seed) return bad("pH and replica_seed arrays are required");
+  if (!finite_arr(prm->pH, R)) return bad("non-finite pH");
+  if (prm->pme_order != 4) { c.err = "only pme_order 4 is implemented"; return fail_create(ctx, CPH_E_UNSUPPORTED); }
+  for (int d = 0; d < 3; ++d)
+    if (prm->pme_grid[d] < 8 || prm->pme_grid[d] % 2 || !smooth2357(prm->pme_grid[d])) {
+      c.err = "PME grid dimensions must be even, >= 8 and 2,3,5,7-smooth";
+      return fail_create(ctx, CPH_E_UNSUPPORTED);
+    }
+  // exclusions
+  std::vector<std::vector<int>> ex(N);
+  if (sys->n_excl < 0 || (sys->n_excl > 0 && !sys->excl)) return bad("bad exclusion list");
+  for (int e = 0; e < sys->n_excl; ++e) {
+    const int a = sys->excl[2 * e], b = sys->excl[2 * e + 1];
+    if (a < 0 || b < 0 || a >= N || b >= N || a == b) return bad("exclusion index out of range or i == j");
+    ex[a].push_back(b);
+    ex[b].push_back(a);
+  }
+  c.h_excl_ptr.assign(N + 1, 0);
+  for (int i = 0; i < N; ++i) {
+    std::sort(ex[i].begin(), ex[i].end());
+    ex[i].erase(std::unique(ex[i].begin(), ex[i].end()), ex[i].end());
+    c.h_excl_ptr[i + 1] = c.h_excl_ptr[i] + (int)ex[i].size();
+    c.h_excl_idx.insert(c.h_excl_idx.end(), ex[i].begin(), ex[i].end());
+  }
+  // lambda groups
+  if (G < 0) return bad("n_groups < 0");
+  int nlam = 0;
+  std::vector<int> lslot(N, -1);
+  c.h_cptr.assign(G + 1, 0);
+  if (G > 0) {
+    if (!sys->group_kind || !sys->group_ptr || !sys->group_atoms || !sys->state_q || !sys->pKa || !sys->vmm)
+      return bad("group arrays are required when n_groups > 0");
+    if (sys->group_ptr[0] != 0) return bad("group_ptr[0] must be 0");
+    for (int g = 0; g < G; ++g) {
+      const int k = sys->group_kind[g];
+      if (k != 2 && k != 3) return bad("group_kind must be 2 or 3");
+      if (sys->group_ptr[g + 1] <= sys->group_ptr[g]) return bad("empty lambda-group");
+      c.h_cptr[g + 1] = c.h_cptr[g] + (k == 2 ? 1 : 2);
+    }
+    nlam = sys->group_ptr[G];
+    if (!finite_arr(sys->state_q, 4 * (size_t)nlam) || !finite_arr(sys->pKa, 3 * (size_t)G) ||
+        !finite_arr(sys->vmm, 36 * (size_t)G))
+      return bad("non-finite group parameter");
+    for (int g = 0; g < G; ++g) {
+      double tot[4] = {0, 0, 0, 0};
+      for (int k = sys->group_ptr[g]; k < sys->group_ptr[g + 1]; ++k) {
+        const int a = sys->group_atoms[k];
+        if (a < 0 || a >= N) return bad("group atom out of range");
+        if (lslot[a] >= 0) return bad("atom belongs to more than one lambda-group");
+        lslot[a] = k;
+        const double *q = sys->state_q + 4 * (size_t)k;
+        for (int s = 0; s < 4; ++s) tot[s] += q[s];
+        if (sys->group_kind[g] == 2 && (std::fabs(q[0] - q[1]) > 1e-12 || std::fabs(q[2] - q[3]) > 1e-12))
+          return bad("2-state group requires q^A == q^B and q^C == q^D");
+      }
+      for (int s = 1; s < 4; ++s)
+        if (std::fabs(tot[s] - tot[0]) > 1e-9)
+          return bad("lambda-group total charge varies between forms (site + buffer must be constant, PAPER.md:817)");
+    }
+    c.h_group_kind.assign(sys->group_kind, sys->group_kind + G);
+    c.h_group_ptr.assign(sys->group_ptr, sys->group_ptr + G + 1);
+    c.h_group_atoms.assign(sys->group_atoms, sys->group_atoms + nlam);
+    c.h_state_q.assign(sys->state_q, sys->state_q + 4 * (size_t)nlam);
+    c.h_pKa.assign(sys->pKa, sys->pKa + 3 * (size_t)G);
+  }
+  const int C = c.h_cptr[G];
+  if (prm->lambda0 && !finite_arr(prm->lambda0, (size_t)R * C)) return bad("non-finite lambda0");
+
+  // ---- kernel parameters ------------------------------------------------------------
+  KParams &kp = c.kp;
+  kp.R = R; kp.N = N; kp.Nst = (N + 31) / 32 * 32;
+  double V = 1.0;
+  for (int d = 0; d < 3; ++d) {
+    kp.Ld[d] = sys->box[d];
+    kp.L[d] = (float)sys->box[d];
+    kp.invL[d] = 1.0f / kp.L[d];
+    V *= sys->box[d];
+  }
+  kp.V = (float)V;
+  {
+    const float rcf = (float)prm->rc, rlf = (float)prm->rlist;
+    kp.rc2 = rcf * rcf;
+    kp.rlist2 = rlf * rlf;
+  }
+  kp.beta_d = erfc_beta(prm->rc, prm->ewald_rtol);
+  kp.beta = (float)kp.beta_d;
+  kp.beta_p = kp.beta * kErfcP;
+  kp.two_beta_sqrtpi = (float)(2.0 * kp.beta_d / std::sqrt(kPi));
+  kp.fcoul = (float)kFCoul;
+  kp.T = T;
+  kp.ncell = 1;
+  for (int d = 0; d < 3; ++d) {
+    int nc = (int)std::floor(sys->box[d] / (0.5 * prm->rlist * (1.0 + 1e-4)));
+    if (nc < 1) nc = 1;
+    kp.nc[d] = nc;
+    if (nc >= 5) { kp.ns[d] = 5; kp.so[d] = -2; }
+    else { kp.ns[d] = nc; kp.so[d] = 0; }
+    kp.ncell *= nc;
+  }
+  {
+    const double expect = (double)N / V * 4.0 / 3.0 * kPi * std::pow(prm->rlist, 3);
+    kp.cap = (int)std::ceil(1.6 * expect + 64.0);
+    kp.cap = (kp.cap + 7) / 8 * 8;
+  }
+  for (int d = 0; d < 3; ++d) kp.K[d] = prm->pme_grid[d];
+  kp.K3 = kp.K[0] * kp.K[1] * kp.K[2];
+  kp.Kzc = kp.K[2] / 2 + 1;
+  kp.Kc = kp.K[0] * kp.K[1] * kp.Kzc;
+  kp.dtd = prm->dt;
+  kp.dt = (float)prm->dt;
+  kp.kT = kBoltz * prm->temperature;
+  kp.kT_f = (float)kp.kT;
+  {
+    const double c1 = std::exp(-prm->gamma_atom * prm->dt);
+    kp.c1_atom = (float)c1;
+    kp.c2_atom_kT = (float)((1.0 - c1 * c1) * kp.kT);
+    const double cl = std::exp(-prm->gamma_lambda * prm->dt);
+    kp.c1_lam = cl;
+    kp.sd_lam = std::sqrt((1.0 - cl * cl) * kp.kT / prm->lambda_mass);
+    kp.m_lam = prm->lambda_mass;
+  }
+  kp.nstout = prm->nstout;
+  kp.nstenergy = prm->nstenergy;
+  kp.nstlist = prm->nstlist;
+  kp.mode = prm->mode;
+  kp.G = G; kp.C = C; kp.nlam = nlam;
+  kp.h_barrier = prm->barrier;
+  kp.wall_k = prm->wall_k;
+  kp.fcap = prm->frame_capacity;
+  kp.Q_fixed = 0.0; kp.Q2_fixed = 0.0;
+  for (int i = 0; i < N; ++i)
+    if (lslot[i] < 0) { kp.Q_fixed += sys->charge[i]; kp.Q2_fixed += (double)sys->charge[i] * sys->charge[i]; }
+
+  // ---- device ------------------------------------------------------------------------
+  c.device = prm->device;
+  if (cudaSetDevice(prm->device) != cudaSuccess) { c.err = "cudaSetDevice failed"; return fail_create(ctx, CPH_E_CUDA); }
+  c.dev_alloc = prm->dev_alloc;
+  c.dev_free = prm->dev_free;
+  c.alloc_ctx = prm->alloc_ctx;
+  if (prm->cuda_stream) c.stream = (cudaStream_t)prm->cuda_stream;
+  else {
+    if (cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess) {
+      c.err = "stream creation failed";
+      return fail_create(ctx, CPH_E_CUDA);
+    }
+    c.own_stream = true;
+  }
+  if (cudaStreamCreateWithFlags(&c.stream_pme, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    c.err = "stream/event creation failed";
+    return fail_create(ctx, CPH_E_CUDA);
+  }
+  DevBufs &d = c.d;
+  const size_t RN = (size_t)R * kp.Nst;
+  d.xyzq = dalloc<float4>(c, RN); d.xyzq_alt = dalloc<float4>(c, RN);
+  d.vel = dalloc<float4>(c, RN); d.vel_alt = dalloc<float4>(c, RN);
+  d.meta = dalloc<int2>(c, RN); d.meta_alt = dalloc<int2>(c, RN);
+  d.f_nb = dalloc<float4>(c, RN); d.f_rec = dalloc<float4>(c, RN);
+  d.iperm = dalloc<int>(c, (size_t)R * N);
+  d.cell_of = dalloc<int>(c, RN); d.cell_rank = dalloc<int>(c, RN);
+  d.cell_count = dalloc<int>(c, (size_t)R * kp.ncell);
+  d.cell_start = dalloc<int>(c, (size_t)R * (kp.ncell + 1));
+  d.perm_tmp = dalloc<int>(c, RN);
+  d.nbl = dalloc<uint32_t>(c, RN * kp.cap);
+  d.nnb = dalloc<int>(c, RN);
+  d.excl_ptr = dalloc<int>(c, N + 1);
+  d.excl_idx = dalloc<int>(c, c.h_excl_idx.size());
+  d.ljtab = dalloc<float2>(c, (size_t)T * T);
+  d.phi64_nb = dalloc<double>(c, (size_t)R * nlam);
+  d.phi64_rec = dalloc<double>(c, (size_t)R * nlam);
+  d.phi_lam = dalloc<double>(c, (size_t)R * nlam);
+  d.grid = dalloc<float>(c, (size_t)R * kp.K3);
+  d.cgrid = dalloc<float2>(c, (size_t)R * kp.Kc);
+  d.bsp = dalloc<float>(c, kp.K[0] + kp.K[1] + kp.K[2]);
+  d.g_kind = dalloc<int>(c, G); d.g_ptr = dalloc<int>(c, G + 1);
+  d.g_atoms = dalloc<int>(c, nlam); d.g_cptr = dalloc<int>(c, G + 1);
+  d.g_q = dalloc<double>(c, 4 * (size_t)nlam);
+  d.vmm = dalloc<double>(c, 36 * (size_t)G);
+  d.g_dG = dalloc<double>(c, (size_t)R * G * 3);
+  d.d1 = dalloc<double>(c, (size_t)R * C);
+  d.lam = dalloc<double>(c, (size_t)R * C); d.lamv = dalloc<double>(c, (size_t)R * C);
+  d.qlam = dalloc<double>(c, (size_t)R * nlam);
+  d.dvdl_coul = dalloc<double>(c, (size_t)R * C); d.dvdl_bias = dalloc<double>(c, (size_t)R * C);
+  d.ti_sum = dalloc<double>(c, (size_t)R * C);
+  d.ti_n = dalloc<long long>(c, 1);
+  d.erec = dalloc<double>(c, 2 * (size_t)R * kNE);
+  d.frames = dalloc<float>(c, (size_t)R * kp.fcap * C);
+  d.frame_total = dalloc<long long>(c, R);
+  d.step = dalloc<long long>(c, 1); d.end_step = dalloc<long long>(c, 1);
+  d.done_counter = dalloc<int>(c, 1);
+  d.flags = dalloc<int>(c, FLAG_COUNT);
+  d.seed = dalloc<uint64_t>(c, R);
+  for (void *p : {(void *)d.xyzq, (void *)d.nbl, (void *)d.grid, (void *)d.cgrid, (void *)d.flags, (void *)d.seed})
+    if (!p) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
+  if (c.allocations.size() < 40) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
+
+  // ---- uploads -----------------------------------------------------------------------
+  std::vector<float4> hx(RN), hv(RN);
+  std::vector<int2> hm(RN);
+  std::vector<int> hperm((size_t)R * N);
+  for (int r = 0; r < R; ++r) {
+    const float *P = prm->pos_replicas ? prm->pos_replicas + (size_t)r * N * 3 : sys->pos;
+    const float *Vv = prm->vel_replicas ? prm->vel_replicas + (size_t)r * N * 3 : sys->vel;
+    if (prm->pos_replicas && !finite_arr(P, 3 * (size_t)N)) return bad("non-finite pos_replicas");
+    if (prm->vel_replicas && !finite_arr(Vv, 3 * (size_t)N)) return bad("non-finite vel_replicas");
+    for (int i = 0; i < N; ++i) {
+      const size_t idx = (size_t)r * kp.Nst + i;
+      const float q = lslot[i] >= 0 ? 0.0f : sys->charge[i];
+      hx[idx] = make_float4(P[3 * i], P[3 * i + 1], P[3 * i + 2], q);
+      const float m = sys->mass[i];
+      const float invm = m > 0.0f ? 1.0f / m : 0.0f;
+      if (Vv && m > 0.0f) hv[idx] = make_float4(Vv[3 * i], Vv[3 * i + 1], Vv[3 * i + 2], invm);
+      else hv[idx] = make_float4(0.f, 0.f, 0.f, invm);
+      hm[idx] = make_int2(i, sys->type[i] | ((lslot[i] + 1) << 8));
+      hperm[(size_t)r * N + i] = i;
+    }
+  }
+  std::vector<float2> lj((size_t)T * T);
+  for (int t = 0; t < T * T; ++t) lj[t] = make_float2((float)(6.0 * sys->c6[t]), (float)(12.0 * sys->c12[t]));
+  std::vector<float> bsp;
+  for (int dd = 0; dd < 3; ++dd) bsp_moduli(kp.K[dd], bsp);
+  std::vector<double> lam0((size_t)R * C, 0.0);
+  if (prm->lambda0) std::copy(prm->lambda0, prm->lambda0 + (size_t)R * C, lam0.begin());
+  c.h_seed.assign(prm->replica_seed, prm->replica_seed + R);
+  c.h_pH.assign(prm->pH, prm->pH + R);
+  c.h_d1.assign((size_t)R * C, 0.0);
+
+#define UP(dst, src, n) CK(cudaMemcpy(dst, src, sizeof(*(src)) * (n), cudaMemcpyHostToDevice))
+  {
+    auto up = [&]() -> cph_status {
+      UP(d.xyzq, hx.data(), RN); UP(d.vel, hv.data(), RN); UP(d.meta, hm.data(), RN);
+      UP(d.iperm, hperm.data(), (size_t)R * N);
+      UP(d.excl_ptr, c.h_excl_ptr.data(), N + 1);
+      if (!c.h_excl_idx.empty()) UP(d.excl_idx, c.h_excl_idx.data(), c.h_excl_idx.size());
+      UP(d.ljtab, lj.data(), lj.size());
+      UP(d.bsp, bsp.data(), bsp.size());
+      if (G) {
+        UP(d.g_kind, c.h_group_kind.data(), G); UP(d.g_ptr, c.h_group_ptr.data(), G + 1);
+        UP(d.g_atoms, c.h_group_atoms.data(), nlam); UP(d.g_cptr, c.h_cptr.data(), G + 1);
+        UP(d.g_q, c.h_state_q.data(), 4 * (size_t)nlam); UP(d.vmm, sys->vmm, 36 * (size_t)G);
+      }
+      if (C) UP(d.lam, lam0.data(), (size_t)R * C);
+      UP(d.seed, c.h_seed.data(), R);
+      return CPH_OK;
+    };
+    cph_status st = up();
+    if (st != CPH_OK) return fail_create(ctx, st);
+  }
+#undef UP
+  for (int r = 0; r < R; ++r) {
+    cph_status st = run_pfc(c, r);
+    if (st != CPH_OK) return fail_create(ctx, st);
+  }
+  // cuFFT plans (batched over replicas)
+  {
+    int n3[3] = {kp.K[0], kp.K[1], kp.K[2]};
+    if (cufftPlanMany(&c.plan_r2c, 3, n3, nullptr, 1, kp.K3, nullptr, 1, kp.Kc, CUFFT_R2C, R) != CUFFT_SUCCESS ||
+        cufftPlanMany(&c.plan_c2r, 3, n3, nullptr, 1, kp.Kc, nullptr, 1, kp.K3, CUFFT_C2R, R) != CUFFT_SUCCESS) {
+      c.err = "cufftPlanMany failed";
+      return fail_create(ctx, CPH_E_CUDA);
+    }
+  }
+  c.host_step = 0;
+  cph_status st = evaluate_here(c);
+  if (st == CPH_OK) st = check_flags(c);
+  if (st != CPH_OK) {
+    cph_status s2 = st;
+    if (c.plan_r2c) cufftDestroy(c.plan_r2c);
+    if (c.plan_c2r) cufftDestroy(c.plan_c2r);
+    return fail_create(ctx, s2);
+  }
+  *out = ctx;
+  return CPH_OK;
+}
+
+void cph_destroy(cph_ctx *ctx) {
+  if (!ctx) return;
+  Ctx &c = ctx->c;
+  cudaSetDevice(c.device);
+  cudaStreamSynchronize(c.stream);
+  if (c.graph_block) cudaGraphExecDestroy(c.graph_block);
+  if (c.plan_r2c) cufftDestroy(c.plan_r2c);
+  if (c.plan_c2r) cufftDestroy(c.plan_c2r);
+  free_all(c);
+  if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+  if (c.ev_join) cudaEventDestroy(c.ev_join);
+  if (c.stream_pme) cudaStreamDestroy(c.stream_pme);
+  if (c.own_stream) cudaStreamDestroy(c.stream);
+  delete ctx;
+}
+
+int32_t cph_n_coords(const cph_ctx *ctx) { return ctx ? ctx->c.kp.C : -1; }
+int32_t cph_n_atoms(const cph_ctx *ctx) { return ctx ? ctx->c.kp.N : -1; }
+int32_t cph_n_replicas(const cph_ctx *ctx) { return ctx ? ctx->c.kp.R : -1; }
+int64_t cph_current_step(const cph_ctx *ctx) { return ctx ? ctx->c.host_step : -1; }
+int64_t cph_launch_count(const cph_ctx *ctx) { return ctx ? ctx->c.launches : -1; }
+
+cph_status cph_set_pH(cph_ctx *ctx, int32_t replica, double pH) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, replica);
+  if (st) return st;
+  if (!std::isfinite(pH)) { c.err = "non-finite pH"; return CPH_E_INVALID; }
+  cudaSetDevice(c.device);
+  CK(cudaStreamSynchronize(c.stream));
+  const double old = c.h_pH[replica];
+  c.h_pH[replica] = pH;
+  st = run_pfc(c, replica);
+  if (st != CPH_OK) c.h_pH[replica] = old;
+  return st;
+}
+
+cph_status cph_step(cph_ctx *ctx, int64_t n_steps) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  if (n_steps < 0) { c.err = "n_steps < 0"; return CPH_E_INVALID; }
+  if (n_steps == 0) return CPH_OK;
+  cudaSetDevice(c.device);
+  const long long end = c.host_step + n_steps;
+  k_set_end<<<1, 1, 0, c.stream>>>(c.d.end_step, end);
+  int k = 1;
+  k += launch_lambda_open(c, c.stream);
+  const int nl = c.kp.nstlist;
+  while (c.host_step < end) {
+    const long long remaining = end - c.host_step;
+    if (c.host_step % nl == 0 && remaining >= nl) {
+      cph_status st = capture_block(c);
+      if (st) return st;
+      CK(cudaGraphLaunch(c.graph_block, c.stream));
+      k += c.graph_block_kernels;
+      c.host_step += nl;
+    } else {
+      k += enqueue_step(c, (c.host_step + 1) % nl == 0, true);
+      c.host_step += 1;
+    }
+  }
+  k += launch_close(c, c.stream, 1);
+  c.launches += k;
+  CK(cudaGetLastError());
+  return CPH_OK;
+}
+
+cph_status cph_sync(cph_ctx *ctx) {
+  if (!ctx) return CPH_E_INVALID;
+  cudaSetDevice(ctx->c.device);
+  return check_flags(ctx->c);
+}
+
+cph_status cph_get_lambdas(cph_ctx *ctx, int32_t r, double *lam, double *vel) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  const size_t C = c.kp.C;
+  if (lam && C) CK(cudaMemcpy(lam, c.d.lam + r * C, sizeof(double) * C, cudaMemcpyDeviceToHost));
+  if (vel && C) CK(cudaMemcpy(vel, c.d.lamv + r * C, sizeof(double) * C, cudaMemcpyDeviceToHost));
+  return CPH_OK;
+}
+
+cph_status cph_get_dvdl(cph_ctx *ctx, int32_t r, double *coul, double *bias) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  const size_t C = c.kp.C;
+  if (coul && C) CK(cudaMemcpy(coul, c.d.dvdl_coul + r * C, sizeof(double) * C, cudaMemcpyDeviceToHost));
+  if (bias && C) CK(cudaMemcpy(bias, c.d.dvdl_bias + r * C, sizeof(double) * C, cudaMemcpyDeviceToHost));
+  return CPH_OK;
+}
+
+cph_status cph_get_bias_params(cph_ctx *ctx, int32_t r, double *d1) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st) return st;
+  if (d1) std::copy(c.h_d1.begin() + (size_t)r * c.kp.C, c.h_d1.begin() + (size_t)(r + 1) * c.kp.C, d1);
+  return CPH_OK;
+}
+
+cph_status cph_get_energies(cph_ctx *ctx, int32_t r, double *e) {
+  if (!ctx || !e) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  const size_t off = ((size_t)(c.host_step & 1) * c.kp.R + r) * kNE;
+  CK(cudaMemcpy(e, c.d.erec + off, sizeof(double) * kNE, cudaMemcpyDeviceToHost));
+  double tot = 0.0;
+  for (int k = 0; k < CPH_E_TOTAL; ++k) tot += e[k];
+  e[CPH_E_TOTAL] = tot;
+  return CPH_OK;
+}
+
+cph_status cph_get_frames(cph_ctx *ctx, int32_t r, float *buf, int64_t cap, int64_t *n_frames, int64_t *n_dropped) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  const KParams &kp = c.kp;
+  long long total = 0;
+  CK(cudaMemcpy(&total, c.d.frame_total + r, sizeof(long long), cudaMemcpyDeviceToHost));
+  const long long avail = std::min<long long>(total, kp.fcap);
+  const long long take = std::min<long long>(avail, cap);
+  std::vector<float> all((size_t)kp.fcap * kp.C);
+  if (kp.C) CK(cudaMemcpy(all.data(), c.d.frames + (size_t)r * kp.fcap * kp.C, sizeof(float) * all.size(), cudaMemcpyDeviceToHost));
+  // oldest retained frame index = total - avail; we return the newest `take` frames in order
+  const long long first = total - take;
+  for (long long f = 0; f < take && buf; ++f) {
+    const long long slot = (first + f) % kp.fcap;
+    for (int k = 0; k < kp.C; ++k) buf[f * kp.C + k] = all[(size_t)slot * kp.C + k];
+  }
+  if (n_frames) *n_frames = take;
+  if (n_dropped) *n_dropped = total - take;
+  const long long zero = 0;
+  CK(cudaMemcpy(c.d.frame_total + r, &zero, sizeof(long long), cudaMemcpyHostToDevice));
+  return CPH_OK;
+}
+
+cph_status cph_get_forces(cph_ctx *ctx, int32_t r, float *f, float *phi) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  const KParams &kp = c.kp;
+  const size_t N = kp.N, base = (size_t)r * kp.Nst;
+  std::vector<float4> nb(N), rec(N), xq(N);
+  std::vector<int2> meta(N);
+  std::vector<double> plam(kp.nlam), qlam(kp.nlam);
+  CK(cudaMemcpy(nb.data(), c.d.f_nb + base, sizeof(float4) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(rec.data(), c.d.f_rec + base, sizeof(float4) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(xq.data(), c.d.xyzq + base, sizeof(float4) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(meta.data(), c.d.meta + base, sizeof(int2) * N, cudaMemcpyDeviceToHost));
+  if (kp.nlam) {
+    CK(cudaMemcpy(plam.data(), c.d.phi_lam + (size_t)r * kp.nlam, sizeof(double) * kp.nlam, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(qlam.data(), c.d.qlam + (size_t)r * kp.nlam, sizeof(double) * kp.nlam, cudaMemcpyDeviceToHost));
+  }
+  double Q = kp.Q_fixed;
+  for (double q : qlam) Q += q;
+  const double V = kp.Ld[0] * kp.Ld[1] * kp.Ld[2];
+  const double phinet = -kPi * Q / (V * kp.beta_d * kp.beta_d);
+  const double selfc = -2.0 * kp.beta_d / std::sqrt(kPi);
+  for (size_t s = 0; s < N; ++s) {
+    const int o = meta[s].x;
+    const int ls = (meta[s].y >> 8) - 1;
+    if (f) {
+      f[3 * o] = nb[s].x + rec[s].x;
+      f[3 * o + 1] = nb[s].y + rec[s].y;
+      f[3 * o + 2] = nb[s].z + rec[s].z;
+    }
+    if (phi) {
+      if (ls >= 0) phi[o] = (float)plam[ls];
+      else phi[o] = (float)((double)nb[s].w + (double)rec[s].w + selfc * xq[s].w + phinet);
+    }
+  }
+  return CPH_OK;
+}
+
+cph_status cph_get_positions(cph_ctx *ctx, int32_t r, float *pos, float *vel) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  const size_t N = c.kp.N, base = (size_t)r * c.kp.Nst;
+  std::vector<float4> xq(N), v(N);
+  std::vector<int2> meta(N);
+  CK(cudaMemcpy(xq.data(), c.d.xyzq + base, sizeof(float4) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(v.data(), c.d.vel + base, sizeof(float4) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(meta.data(), c.d.meta + base, sizeof(int2) * N, cudaMemcpyDeviceToHost));
+  for (size_t s = 0; s < N; ++s) {
+    const int o = meta[s].x;
+    if (pos) { pos[3 * o] = xq[s].x; pos[3 * o + 1] = xq[s].y; pos[3 * o + 2] = xq[s].z; }
+    if (vel) { vel[3 * o] = v[s].x; vel[3 * o + 1] = v[s].y; vel[3 * o + 2] = v[s].z; }
+  }
+  return CPH_OK;
+}
+
+cph_status cph_get_pairlist(cph_ctx *ctx, int32_t r, int32_t *pairs, int64_t cap, int64_t *n) {
+  if (!ctx || !n) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  const KParams &kp = c.kp;
+  const size_t N = kp.N, base = (size_t)r * kp.Nst;
+  std::vector<int> nnb(N);
+  std::vector<int2> meta(N);
+  std::vector<uint32_t> nbl((size_t)kp.cap * kp.Nst);
+  CK(cudaMemcpy(nnb.data(), c.d.nnb + base, sizeof(int) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(meta.data(), c.d.meta + base, sizeof(int2) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(nbl.data(), c.d.nbl + (size_t)r * kp.cap * kp.Nst, sizeof(uint32_t) * nbl.size(), cudaMemcpyDeviceToHost));
+  std::vector<std::pair<int, int>> out;
+  for (size_t i = 0; i < N; ++i) {
+    const int oi = meta[i].x;
+    for (int k = 0; k < std::min(nnb[i], kp.cap); ++k) {
+      const int j = (int)(nbl[(size_t)k * kp.Nst + i] & 0xFFFFFFu);
+      const int oj = meta[j].x;
+      if (oi < oj) out.emplace_back(oi, oj);
+    }
+  }
+  std::sort(out.begin(), out.end());
+  *n = (int64_t)out.size();
+  if (pairs && cap >= (int64_t)out.size())
+    for (size_t k = 0; k < out.size(); ++k) { pairs[2 * k] = out[k].first; pairs[2 * k + 1] = out[k].second; }
+  return CPH_OK;
+}
+
+cph_status cph_get_ti_means(cph_ctx *ctx, int32_t r, double *mean, int64_t *n_samples) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  long long n = 0;
+  CK(cudaMemcpy(&n, c.d.ti_n, sizeof(long long), cudaMemcpyDeviceToHost));
+  std::vector<double> s(c.kp.C);
+  if (c.kp.C) CK(cudaMemcpy(s.data(), c.d.ti_sum + (size_t)r * c.kp.C, sizeof(double) * c.kp.C, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < c.kp.C && mean; ++k) mean[k] = n ? s[k] / (double)n : 0.0;
+  if (n_samples) *n_samples = n;
+  return CPH_OK;
+}
+
+// blob: int64 magic, N, C, step | float pos[3N], vel[3N] | double lam[C], lamv[C]
+static const int64_t kMagic = 0x3148504331ll;
+
+cph_status cph_get_state(cph_ctx *ctx, int32_t r, void *buf, int64_t cap, int64_t *n) {
+  if (!ctx || !n) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st) return st;
+  const size_t N = c.kp.N, C = c.kp.C;
+  const size_t bytes = 4 * sizeof(int64_t) + 6 * N * sizeof(float) + 2 * C * sizeof(double);
+  *n = (int64_t)bytes;
+  if (!buf) return CPH_OK;
+  if (cap < (int64_t)bytes) { c.err = "state buffer too small"; return CPH_E_INVALID; }
+  char *p = (char *)buf;
+  int64_t hdr[4] = {kMagic, (int64_t)N, (int64_t)C, c.host_step};
+  std::memcpy(p, hdr, sizeof hdr);
+  float *pos = (float *)(p + sizeof hdr);
+  if ((st = cph_get_positions(ctx, r, pos, pos + 3 * N))) return st;
+  double *lam = (double *)(pos + 6 * N);
+  return cph_get_lambdas(ctx, r, lam, lam + C);
+}
+
+cph_status cph_set_state(cph_ctx *ctx, int32_t r, const void *buf, int64_t nbytes) {
+  if (!ctx || !buf) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  const size_t N = c.kp.N, C = c.kp.C;
+  const size_t bytes = 4 * sizeof(int64_t) + 6 * N * sizeof(float) + 2 * C * sizeof(double);
+  int64_t hdr[4];
+  if (nbytes < (int64_t)bytes) { c.err = "state blob too small"; return CPH_E_INVALID; }
+  std::memcpy(hdr, buf, sizeof hdr);
+  if (hdr[0] != kMagic || hdr[1] != (int64_t)N || hdr[2] != (int64_t)C) {
+    c.err = "state blob does not match this context";
+    return CPH_E_INVALID;
+  }
+  const float *pos = (const float *)((const char *)buf + sizeof hdr);
+  const float *vel = pos + 3 * N;
+  const double *lam = (const double *)(vel + 3 * N);
+  if (!finite_arr(pos, 6 * N) || !finite_arr(lam, 2 * C)) { c.err = "non-finite state"; return CPH_E_INVALID; }
+  const size_t base = (size_t)r * c.kp.Nst;
+  std::vector<float4> xq(N), v(N);
+  std::vector<int2> meta(N);
+  CK(cudaMemcpy(xq.data(), c.d.xyzq + base, sizeof(float4) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(v.data(), c.d.vel + base, sizeof(float4) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(meta.data(), c.d.meta + base, sizeof(int2) * N, cudaMemcpyDeviceToHost));
+  for (size_t s = 0; s < N; ++s) {
+    const int o = meta[s].x;
+    xq[s].x = pos[3 * o]; xq[s].y = pos[3 * o + 1]; xq[s].z = pos[3 * o + 2];
+    if (v[s].w > 0.0f) { v[s].x = vel[3 * o]; v[s].y = vel[3 * o + 1]; v[s].z = vel[3 * o + 2]; }
+  }
+  CK(cudaMemcpy(c.d.xyzq + base, xq.data(), sizeof(float4) * N, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c.d.vel + base, v.data(), sizeof(float4) * N, cudaMemcpyHostToDevice));
+  if (C) {
+    CK(cudaMemcpy(c.d.lam + (size_t)r * C, lam, sizeof(double) * C, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c.d.lamv + (size_t)r * C, lam + C, sizeof(double) * C, cudaMemcpyHostToDevice));
+  }
+  st = evaluate_here(c);
+  if (st) return st;
+  return check_flags(c);
+}
+
+cph_status cph_profile_steps(cph_ctx *ctx, int64_t n_steps, double *ms, int64_t *launches) {
+  if (!ctx || n_steps < 0) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cudaSetDevice(c.device);
+  cudaStream_t s = c.stream;
+  std::vector<cudaEvent_t> evs;
+  std::vector<int> cls;
+  auto mark = [&](int k) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    evs.push_back(e);
+    cls.push_back(k);
+  };
+  int64_t cnt[CPH_N_KCLASSES] = {0};
+  const long long end = c.host_step + n_steps;
+  k_set_end<<<1, 1, 0, s>>>(c.d.end_step, end);
+  int k = 1;
+  mark(-1);
+  k += launch_lambda_open(c, s); cnt[CPH_K_LAMBDA] += 1;
+  mark(CPH_K_LAMBDA);
+  cufftSetStream(c.plan_r2c, s);
+  cufftSetStream(c.plan_c2r, s);
+  while (c.host_step < end) {
+    const bool rebuild = (c.host_step + 1) % c.kp.nstlist == 0;
+    k += launch_integrate(c, s, 1); cnt[CPH_K_INTEGRATE] += 1; mark(CPH_K_INTEGRATE);
+    if (rebuild) { int q = launch_rebuild(c, s); k += q; cnt[CPH_K_PAIRLIST] += q; mark(CPH_K_PAIRLIST); }
+    k += launch_nonbonded(c, s, 1); cnt[CPH_K_NONBONDED] += 1; mark(CPH_K_NONBONDED);
+    k += launch_spread(c, s); cnt[CPH_K_SPREAD] += 1; mark(CPH_K_SPREAD);
+    cufftExecR2C(c.plan_r2c, c.d.grid, (cufftComplex *)c.d.cgrid); mark(CPH_K_FFT_R2C);
+    k += launch_solve(c, s, 1); cnt[CPH_K_SOLVE] += 1; mark(CPH_K_SOLVE);
+    cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid); mark(CPH_K_FFT_C2R);
+    k += launch_gather(c, s); cnt[CPH_K_GATHER] += 1; mark(CPH_K_GATHER);
+    k += launch_lambda_reduce(c, s, 1); cnt[CPH_K_LAMBDA] += 1; mark(CPH_K_LAMBDA);
+    c.host_step += 1;
+  }
+  k += launch_close(c, s, 1); cnt[CPH_K_INTEGRATE] += 1; mark(CPH_K_INTEGRATE);
+  c.launches += k;
+  CK(cudaStreamSynchronize(s));
+  double acc[CPH_N_KCLASSES] = {0};
+  for (size_t e = 1; e < evs.size(); ++e) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, evs[e - 1], evs[e]);
+    acc[cls[e]] += t;
+  }
+  for (auto e : evs) cudaEventDestroy(e);
+  if (ms) for (int q = 0; q < CPH_N_KCLASSES; ++q) ms[q] = acc[q];
+  if (launches) for (int q = 0; q < CPH_N_KCLASSES; ++q) launches[q] = cnt[q];
+  CK(cudaGetLastError());
+  return check_flags(c);
+}
+
+}  // extern "C"

@@ -1,0 +1,280 @@
+// Atom and lambda-particle integration and the lambda-group reduction.
+//
+// BAOAB (R9): B v += dt/2 F/m ; A x += dt/2 v ; O v = c1 v + sqrt((1-c1^2) kT/m) xi ;
+// A x += dt/2 v ; forces at (x, lambda) ; B v += dt/2 F/m.  The closing B of step n is fused
+// into the opening of step n+1 (FLAG_PENDING_CLOSE) and finished by k_close at the end of a
+// cph_step call, so atom data is read and written once per step.
+#include "cph_device.cuh"
+
+namespace cph {
+
+__global__ void __launch_bounds__(128) k_integrate(KParams kp, DevBufs d) {
+  const int r = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = *d.step;
+  const long long end = *d.end_step;
+  const int pending = d.flags[FLAG_PENDING_CLOSE];
+  if (blockIdx.x == 0 && threadIdx.x < kNE)   // record of step n+1 starts empty
+    d.erec[((size_t)((n + 1) & 1) * kp.R + r) * kNE + threadIdx.x] = 0.0;
+  double ke = 0.0;
+  if (i < kp.N) {
+    const size_t idx = (size_t)r * kp.Nst + i;
+    float4 v = d.vel[idx];
+    const float invm = v.w;
+    if (invm > 0.0f) {
+      float4 x = d.xyzq[idx];
+      const float4 fa = d.f_nb[idx], fb = d.f_rec[idx];
+      const float fx = fa.x + fb.x, fy = fa.y + fb.y, fz = fa.z + fb.z;
+      const float hk = 0.5f * kp.dt * invm;
+      if (pending) {
+        v.x = fmaf(hk, fx, v.x); v.y = fmaf(hk, fy, v.y); v.z = fmaf(hk, fz, v.z);
+        ke = 0.5 * ((double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z) / invm;
+      }
+      v.x = fmaf(hk, fx, v.x); v.y = fmaf(hk, fy, v.y); v.z = fmaf(hk, fz, v.z);      // B
+      const float hdt = 0.5f * kp.dt;
+      x.x = fmaf(hdt, v.x, x.x); x.y = fmaf(hdt, v.y, x.y); x.z = fmaf(hdt, v.z, x.z);  // A
+      const int orig = d.meta[idx].x;
+      const float3 xi = atom_normals(d.seed[r], (uint32_t)n, (uint32_t)orig);
+      const float sd = sqrtf(kp.c2_atom_kT * invm);
+      v.x = fmaf(kp.c1_atom, v.x, sd * xi.x);                                           // O
+      v.y = fmaf(kp.c1_atom, v.y, sd * xi.y);
+      v.z = fmaf(kp.c1_atom, v.z, sd * xi.z);
+      x.x = fmaf(hdt, v.x, x.x); x.y = fmaf(hdt, v.y, x.y); x.z = fmaf(hdt, v.z, x.z);  // A
+      d.xyzq[idx] = x;
+      d.vel[idx] = v;
+    }
+  }
+  if (pending && is_energy_step(n, end, kp.nstenergy))
+    block_atomic_add_d(ke, &d.erec[((size_t)(n & 1) * kp.R + r) * kNE + CPH_E_KE_ATOMS]);
+}
+
+// closing half kick (kick = 1) and/or kinetic energy of the current velocities
+__global__ void __launch_bounds__(128) k_close(KParams kp, DevBufs d, int kick) {
+  const int r = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = *d.step;
+  double ke = 0.0;
+  if (i < kp.N) {
+    const size_t idx = (size_t)r * kp.Nst + i;
+    float4 v = d.vel[idx];
+    if (v.w > 0.0f) {
+      if (kick) {
+        const float4 fa = d.f_nb[idx], fb = d.f_rec[idx];
+        const float hk = 0.5f * kp.dt * v.w;
+        v.x = fmaf(hk, fa.x + fb.x, v.x); v.y = fmaf(hk, fa.y + fb.y, v.y); v.z = fmaf(hk, fa.z + fb.z, v.z);
+        d.vel[idx] = v;
+      }
+      ke = 0.5 * ((double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z) / v.w;
+    }
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) d.flags[FLAG_PENDING_CLOSE] = 0;
+  block_atomic_add_d(ke, &d.erec[((size_t)(n & 1) * kp.R + r) * kNE + CPH_E_KE_ATOMS]);
+}
+
+// ---- lambda helpers ---------------------------------------------------------------------
+// charges of every lambda atom of replica r from its group's (lp, lt) (Eq. 2)
+__device__ void lambda_set_charges(const KParams &kp, const DevBufs &d, int r) {
+  for (int g = threadIdx.x; g < kp.G; g += blockDim.x) {
+    const int c0 = d.g_cptr[g];
+    const double lp = d.lam[(size_t)r * kp.C + c0];
+    const double lt = d.g_kind[g] == 3 ? d.lam[(size_t)r * kp.C + c0 + 1] : 0.0;
+    const double wA = (1.0 - lp) * (1.0 - lt), wB = (1.0 - lp) * lt, wC = lp * (1.0 - lt), wD = lp * lt;
+    for (int k = d.g_ptr[g]; k < d.g_ptr[g + 1]; ++k) {
+      const double *qs = d.g_q + 4 * (size_t)k;
+      const double q = wA * qs[0] + wB * qs[1] + wC * qs[2] + wD * qs[3];
+      d.qlam[(size_t)r * kp.nlam + k] = q;
+      const int slot = d.iperm[(size_t)r * kp.N + d.g_atoms[k]];
+      d.xyzq[(size_t)r * kp.Nst + slot].w = (float)q;
+    }
+  }
+}
+
+// BAOA for lambda coordinates of replica r with noise index `step`, then new charges
+__device__ void lambda_open(const KParams &kp, const DevBufs &d, int r, long long step) {
+  for (int c = threadIdx.x; c < kp.C; c += blockDim.x) {
+    const size_t ix = (size_t)r * kp.C + c;
+    const double F = -(d.dvdl_coul[ix] + d.dvdl_bias[ix]);
+    const double h = kp.dtd;
+    double v = d.lamv[ix], l = d.lam[ix];
+    v += 0.5 * h * F / kp.m_lam;                                              // B
+    l += 0.5 * h * v;                                                         // A
+    v = kp.c1_lam * v + kp.sd_lam * lambda_normal(d.seed[r], (uint32_t)step, (uint32_t)c);  // O
+    l += 0.5 * h * v;                                                         // A
+    d.lamv[ix] = v;
+    d.lam[ix] = l;
+  }
+  __syncthreads();
+  lambda_set_charges(kp, d, r);
+}
+
+__device__ double block_sum_d(double v) {
+  __shared__ double red[32];
+  __shared__ double tot;
+  v = warp_sum_d(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    double s = lane < nw ? red[lane] : 0.0;
+    s = warp_sum_d(s);
+    if (lane == 0) tot = s;
+  }
+  __syncthreads();
+  const double out = tot;
+  __syncthreads();
+  return out;
+}
+
+// One CTA per replica.  mode 0: evaluation at create/set_state (step index = *step, no
+// integration); mode 1: end of a step (index m = *step + 1): dV/dlambda, bias, closing B,
+// frames, energies, then (unless m is the call's last step) the next BAOA + charges.
+__global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, int mode) {
+  const int r = blockIdx.x;
+  const long long n = *d.step;
+  const long long m = mode == 1 ? n + 1 : n;
+  const long long end = *d.end_step;
+  const bool energy = is_energy_step(m, end, kp.nstenergy);
+  const bool dyn = kp.mode == 0;
+  const double f = kFCoul;
+  const double V = kp.Ld[0] * kp.Ld[1] * kp.Ld[2];
+  const double sqrtpi = 1.7724538509055160273;
+
+  // total charge and sum of squares
+  double qs = 0.0, qq = 0.0;
+  for (int k = threadIdx.x; k < kp.nlam; k += blockDim.x) {
+    const double q = d.qlam[(size_t)r * kp.nlam + k];
+    qs += q; qq += q * q;
+  }
+  const double Q = kp.Q_fixed + block_sum_d(qs);
+  const double Q2 = kp.Q2_fixed + block_sum_d(qq);
+  // full potential of each lambda atom (real + excl + recip + self + net)
+  for (int k = threadIdx.x; k < kp.nlam; k += blockDim.x) {
+    const size_t ix = (size_t)r * kp.nlam + k;
+    const double q = d.qlam[ix];
+    d.phi_lam[ix] = d.phi64_nb[ix] + d.phi64_rec[ix] - 2.0 * kp.beta_d / sqrtpi * q -
+                    kPi * Q / (V * kp.beta_d * kp.beta_d);
+  }
+  __syncthreads();
+  // per group: Coulomb dV/dlambda and bias
+  double ebias = 0.0;
+  for (int g = threadIdx.x; g < kp.G; g += blockDim.x) {
+    const int kind = d.g_kind[g];
+    const int c0 = d.g_cptr[g];
+    const size_t ic = (size_t)r * kp.C + c0;
+    const double lp = d.lam[ic];
+    const double lt = kind == 3 ? d.lam[ic + 1] : 0.0;
+    double sp = 0.0, st = 0.0;
+    for (int k = d.g_ptr[g]; k < d.g_ptr[g + 1]; ++k) {
+      const double *q4 = d.g_q + 4 * (size_t)k;
+      const double phi = d.phi_lam[(size_t)r * kp.nlam + k];
+      sp += ((1.0 - lt) * (q4[2] - q4[0]) + lt * (q4[3] - q4[1])) * phi;
+      st += ((1.0 - lp) * (q4[1] - q4[0]) + lp * (q4[3] - q4[2])) * phi;
+    }
+    // bias (Eq. 3): Vmm + VpH + Vdw
+    double vm, vmp, vmt;
+    vmm_eval(d.vmm + 36 * (size_t)g, lp, lt, &vm, &vmp, &vmt);
+    const double *dG = d.g_dG + ((size_t)r * kp.G + g) * 3;
+    double vph, vphp, vpht;
+    if (kind == 2) { vph = lp * dG[0]; vphp = dG[0]; vpht = 0.0; }
+    else {
+      vph = lp * ((1.0 - lt) * dG[1] + lt * dG[2]);
+      vphp = (1.0 - lt) * dG[1] + lt * dG[2];
+      vpht = lp * (dG[2] - dG[1]);
+    }
+    double vd, vdp;
+    vdw_eval(lp, kp.h_barrier, d.d1[ic], kp.wall_k, &vd, &vdp);
+    d.dvdl_coul[ic] = f * sp;
+    d.dvdl_bias[ic] = vmp + vphp + vdp;
+    ebias += vm + vph + vd;
+    if (kind == 3) {
+      double vd2, vdt;
+      vdw_eval(lt, kp.h_barrier, d.d1[ic + 1], kp.wall_k, &vd2, &vdt);
+      d.dvdl_coul[ic + 1] = f * st;
+      d.dvdl_bias[ic + 1] = vmt + vpht + vdt;
+      ebias += vd2;
+    }
+  }
+  ebias = block_sum_d(ebias);   // includes __syncthreads: dV/dlambda visible to the block
+  // closing half kick, frames, TI accumulation, divergence
+  double kel = 0.0;
+  const bool frame = (m % kp.nstout) == 0 && (mode == 1 || (m == 0 && d.frame_total[r] == 0));
+  long long fslot = 0;
+  if (frame) fslot = d.frame_total[r] % kp.fcap;
+  for (int c = threadIdx.x; c < kp.C; c += blockDim.x) {
+    const size_t ix = (size_t)r * kp.C + c;
+    const double dv = d.dvdl_coul[ix] + d.dvdl_bias[ix];
+    double v = d.lamv[ix];
+    const double l = d.lam[ix];
+    if (dyn && mode == 1) {
+      v += 0.5 * kp.dtd * (-dv) / kp.m_lam;
+      d.lamv[ix] = v;
+    }
+    kel += 0.5 * kp.m_lam * v * v;
+    if (frame) d.frames[((size_t)r * kp.fcap + fslot) * kp.C + c] = (float)l;
+    if (!dyn && mode == 1) d.ti_sum[ix] += dv;
+    if (!(fabs(l) <= 10.0) || !isfinite(dv)) atomicOr(&d.flags[FLAG_DIVERGED], 1);
+  }
+  kel = block_sum_d(kel);
+  if (threadIdx.x == 0) {
+    if (frame) d.frame_total[r] += 1;
+    if (energy) {
+      double *e = d.erec + ((size_t)(m & 1) * kp.R + r) * kNE;
+      e[CPH_E_SELF] = -f * kp.beta_d / sqrtpi * Q2;
+      e[CPH_E_NET] = -f * kPi * Q * Q / (2.0 * V * kp.beta_d * kp.beta_d);
+      e[CPH_E_BIAS] = ebias;
+      e[CPH_E_KE_LAMBDA] = dyn ? kel : 0.0;
+    }
+  }
+  __syncthreads();
+  if (mode == 1) {
+    if (dyn && m != end) lambda_open(kp, d, r, m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int t = atomicAdd(d.done_counter, 1);
+      if (t == kp.R - 1) {           // last replica CTA: advance the step counter
+        *d.step = m;
+        *d.done_counter = 0;
+        d.flags[FLAG_PENDING_CLOSE] = 1;
+        if (!dyn) *d.ti_n += 1;
+        __threadfence();
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lambda_open(KParams kp, DevBufs d) {
+  if (kp.mode != 0) return;
+  lambda_open(kp, d, blockIdx.x, *d.step);
+}
+
+__global__ void __launch_bounds__(256) k_set_charges(KParams kp, DevBufs d) {
+  lambda_set_charges(kp, d, blockIdx.x);
+}
+
+// ---- launchers ------------------------------------------------------------------------
+int launch_integrate(Ctx &c, cudaStream_t s, int) {
+  dim3 grid((c.kp.N + 127) / 128, c.kp.R);
+  k_integrate<<<grid, 128, 0, s>>>(c.kp, c.d);
+  return 1;
+}
+int launch_close(Ctx &c, cudaStream_t s, int kick) {
+  dim3 grid((c.kp.N + 127) / 128, c.kp.R);
+  k_close<<<grid, 128, 0, s>>>(c.kp, c.d, kick);
+  return 1;
+}
+int launch_lambda_reduce(Ctx &c, cudaStream_t s, int mode) {
+  k_lambda_reduce<<<c.kp.R, 256, 0, s>>>(c.kp, c.d, mode);
+  return 1;
+}
+int launch_lambda_open(Ctx &c, cudaStream_t s) {
+  k_lambda_open<<<c.kp.R, 256, 0, s>>>(c.kp, c.d);
+  return 1;
+}
+int launch_set_charges(Ctx &c, cudaStream_t s) {
+  k_set_charges<<<c.kp.R, 256, 0, s>>>(c.kp, c.d);
+  return 1;
+}
+
+}  // namespace cph

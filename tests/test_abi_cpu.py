@@ -1,0 +1,70 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol include/cph.h
+declares, and rejects invalid input before touching a device."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def cph():
+    from paper_2410_01626_b200 import build
+    build.build()
+    import paper_2410_01626_b200 as m
+    return m
+
+
+def test_every_header_symbol_is_exported(cph):
+    hdr = open(os.path.join(ROOT, "include", "cph.h")).read()
+    names = set(re.findall(r"\b(cph_[a-z_A-Z0-9]+)\s*\(", hdr))
+    assert len(names) >= 20
+    lib = cph.lib()
+    for n in sorted(names):
+        assert hasattr(lib, n), n
+    assert set(names) == set(cph.binding.EXPORTS)
+
+
+def test_sm100a_code_in_library():
+    import subprocess
+    so = os.path.join(ROOT, "paper_2410_01626_b200", "libcph.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _sys():
+    from synthetic.systems import small_system
+    return small_system()
+
+
+@pytest.mark.parametrize("mutate,msg", [
+    (lambda s: s.pos.__setitem__((0, 0), np.nan), "non-finite"),
+    (lambda s: s.state_q.__setitem__((0, slice(2, 4)), s.state_q[0, 2:4] + 0.1), "total charge"),
+    (lambda s: s.group_kind.__setitem__(0, 4), "group_kind"),
+    (lambda s: s.type.__setitem__(0, 99), "type out of range"),
+    (lambda s: s.excl.__setitem__((0, 1), s.excl[0, 0]), "exclusion"),
+])
+def test_invalid_system_rejected(cph, mutate, msg):
+    s = _sys()
+    mutate(s)
+    with pytest.raises(cph.CphError) as ei:
+        cph.cph_create(s, [4.0], [1], use_torch_allocator=False)
+    assert ei.value.status == 1 and msg in str(ei.value)
+
+
+def test_invalid_params_rejected(cph):
+    s = _sys()
+    with pytest.raises(cph.CphError) as ei:
+        cph.cph_create(s, [4.0], [1], rlist=1.2, use_torch_allocator=False)      # box 2.3 -> rlist >= L/2
+    assert ei.value.status == 1
+    with pytest.raises(cph.CphError) as ei:
+        cph.cph_create(s, [4.0], [1], pme_order=6, use_torch_allocator=False)
+    assert ei.value.status == 6
+    with pytest.raises(cph.CphError) as ei:
+        cph.cph_create(s, [4.0], [1], pme_grid=(22, 22, 22), use_torch_allocator=False)   # 11 not smooth
+    assert ei.value.status == 6
+    with pytest.raises(cph.CphError) as ei:
+        cph.cph_create(s, [np.nan], [1], use_torch_allocator=False)
+    assert ei.value.status == 1
