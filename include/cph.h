@@ -193,6 +193,11 @@ cph_status cph_get_ti_means(cph_ctx *ctx, int32_t replica, double *mean /*[C]*/,
 cph_status cph_get_state(cph_ctx *ctx, int32_t replica, void *buf, int64_t cap, int64_t *n);
 cph_status cph_set_state(cph_ctx *ctx, int32_t replica, const void *buf, int64_t n);
 
+/* All replicas at once (blob = R consecutive per-replica blobs of cph_get_state);
+ * cph_set_state_all re-evaluates forces once for the whole batch. */
+cph_status cph_get_state_all(cph_ctx *ctx, void *buf, int64_t cap, int64_t *n);
+cph_status cph_set_state_all(cph_ctx *ctx, const void *buf, int64_t n);
+
 /* Run n_steps eagerly with CUDA events around every kernel class (serialised,
  * one stream) and return the summed milliseconds per class [CPH_N_KCLASSES]
  * and the number of launches per class [CPH_N_KCLASSES] (either may be NULL). */

@@ -74,6 +74,8 @@ EXPORTS = {
     "cph_get_ti_means": (C.c_int, [C.c_void_p, C.c_int32, _f64p, _i64p]),
     "cph_get_state": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, _i64p]),
     "cph_set_state": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]),
+    "cph_get_state_all": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, _i64p]),
+    "cph_set_state_all": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
     "cph_profile_steps": (C.c_int, [C.c_void_p, C.c_int64, _f64p, _i64p]),
     "cph_launch_count": (C.c_int64, [C.c_void_p]),
     "cph_last_error": (C.c_char_p, [C.c_void_p]),
@@ -312,6 +314,17 @@ class Context:
     def cph_set_state(self, r, blob):
         blob = np.ascontiguousarray(blob, np.uint8)
         _check(lib().cph_set_state(self.h, r, blob.ctypes.data_as(C.c_void_p), blob.size), self.h)
+
+    def cph_get_state_all(self, out=None):
+        n = C.c_int64()
+        _check(lib().cph_get_state_all(self.h, None, 0, C.byref(n)), self.h)
+        buf = np.zeros(n.value, np.uint8) if out is None else out
+        _check(lib().cph_get_state_all(self.h, buf.ctypes.data_as(C.c_void_p), buf.size, C.byref(n)), self.h)
+        return buf
+
+    def cph_set_state_all(self, blob):
+        blob = np.ascontiguousarray(blob, np.uint8)
+        _check(lib().cph_set_state_all(self.h, blob.ctypes.data_as(C.c_void_p), blob.size), self.h)
 
     def cph_profile_steps(self, n):
         ms = np.zeros(len(KERNEL_CLASSES))

@@ -832,11 +832,7 @@ cph_status cph_get_state(cph_ctx *ctx, int32_t r, void *buf, int64_t cap, int64_
   return cph_get_lambdas(ctx, r, lam, lam + C);
 }
 
-cph_status cph_set_state(cph_ctx *ctx, int32_t r, const void *buf, int64_t nbytes) {
-  if (!ctx || !buf) return CPH_E_INVALID;
-  Ctx &c = ctx->c;
-  cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+static cph_status upload_state(Ctx &c, int32_t r, const void *buf, int64_t nbytes) {
   const size_t N = c.kp.N, C = c.kp.C;
   const size_t bytes = 4 * sizeof(int64_t) + 6 * N * sizeof(float) + 2 * C * sizeof(double);
   int64_t hdr[4];
@@ -867,8 +863,43 @@ cph_status cph_set_state(cph_ctx *ctx, int32_t r, const void *buf, int64_t nbyte
     CK(cudaMemcpy(c.d.lam + (size_t)r * C, lam, sizeof(double) * C, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c.d.lamv + (size_t)r * C, lam + C, sizeof(double) * C, cudaMemcpyHostToDevice));
   }
-  st = evaluate_here(c);
+  return CPH_OK;
+}
+
+cph_status cph_set_state(cph_ctx *ctx, int32_t r, const void *buf, int64_t nbytes) {
+  if (!ctx || !buf) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  if ((st = upload_state(c, r, buf, nbytes))) return st;
+  if ((st = evaluate_here(c))) return st;
+  return check_flags(c);
+}
+
+cph_status cph_get_state_all(cph_ctx *ctx, void *buf, int64_t cap, int64_t *n) {
+  if (!ctx || !n) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  int64_t one = 0;
+  cph_status st = cph_get_state(ctx, 0, nullptr, 0, &one);
   if (st) return st;
+  *n = one * c.kp.R;
+  if (!buf) return CPH_OK;
+  if (cap < *n) { c.err = "state buffer too small"; return CPH_E_INVALID; }
+  for (int r = 0; r < c.kp.R; ++r)
+    if ((st = cph_get_state(ctx, r, (char *)buf + (size_t)r * one, one, &one))) return st;
+  return CPH_OK;
+}
+
+cph_status cph_set_state_all(cph_ctx *ctx, const void *buf, int64_t nbytes) {
+  if (!ctx || !buf) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  int64_t one = 0;
+  cph_status st = cph_get_state(ctx, 0, nullptr, 0, &one);
+  if (st || (st = cph_sync(ctx))) return st;
+  if (nbytes < one * c.kp.R) { c.err = "state blob too small"; return CPH_E_INVALID; }
+  for (int r = 0; r < c.kp.R; ++r)
+    if ((st = upload_state(c, r, (const char *)buf + (size_t)r * one, one))) return st;
+  if ((st = evaluate_here(c))) return st;
   return check_flags(c);
 }
 

@@ -1,0 +1,113 @@
+"""Titration bookkeeping on the host.
+
+* replicas = pH points x seeds, dealt round-robin to ranks (one process per GPU; the
+  path shards as independent replicas, so there is no collective
+  inside the step loop);
+* one all-gather of the lambda frames at the end (NCCL over NVLink on GPUs, gloo on
+  CPU), the only collective of a run;
+* deprotonated fraction x = N(lambda_p >= 0.5)/N per replica (PAPER.md:975-978,
+  reading R1), Henderson-Hasselbalch / Hill fit by damped
+  Gauss-Newton, bootstrap over replicas.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def assign_replicas(n_replicas: int, world: int, rank: int):
+    """Round-robin replica indices of one rank."""
+    return list(range(rank, n_replicas, world))
+
+
+def gather_frames(local: np.ndarray, group=None, device=None):
+    """All-gather a per-rank array [R_local, F, C] (padded to the largest R_local) over
+    torch.distributed; returns the concatenation over ranks (every rank gets it)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return np.asarray(local)
+    world = dist.get_world_size(group)
+    backend = dist.get_backend(group)
+    dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
+                                             if backend == "nccl" else torch.device("cpu"))
+    local = np.asarray(local, np.float32)
+    n_local = torch.tensor([local.shape[0]], device=dev, dtype=torch.int64)
+    counts = [torch.zeros_like(n_local) for _ in range(world)]
+    dist.all_gather(counts, n_local, group=group)
+    counts = [int(c.item()) for c in counts]
+    rmax = max(counts)
+    pad = np.zeros((rmax,) + local.shape[1:], np.float32)
+    pad[: local.shape[0]] = local
+    t = torch.from_numpy(pad).to(dev)
+    out = torch.empty((world * rmax,) + tuple(local.shape[1:]), dtype=t.dtype, device=dev)
+    dist.all_gather_into_tensor(out, t, group=group)
+    out = out.cpu().numpy().reshape((world, rmax) + local.shape[1:])
+    return np.concatenate([out[k, : counts[k]] for k in range(world)], 0)
+
+
+def deprotonated_fraction(lambda_p_frames) -> float:
+    lp = np.asarray(lambda_p_frames, np.float64)
+    if lp.size == 0 or not np.all(np.isfinite(lp)):
+        raise ValueError("need finite lambda frames")
+    return float(np.count_nonzero(lp >= 0.5)) / lp.size
+
+
+def _model(pH, pKa, n):
+    return 1.0 / (np.power(10.0, n * (pKa - pH)) + 1.0)
+
+
+def fit_curve(pH, x, hill=False, iters=200):
+    """Least squares of x = 1/(10^(n (pKa - pH)) + 1) by Levenberg-Marquardt with the
+    analytic Jacobian.  Returns pKa (and n when hill=True)."""
+    pH = np.asarray(pH, np.float64)
+    x = np.asarray(x, np.float64)
+    if np.all(x == x[0]):
+        raise ValueError("unidentifiable fit: all fractions equal")
+    p = np.array([pH[np.argmin(np.abs(x - 0.5))], 1.0])
+    mu = 1e-3
+    ln10 = np.log(10.0)
+
+    def resid(v):
+        return _model(pH, v[0], v[1]) - x
+    r = resid(p)
+    for _ in range(iters):
+        y = _model(pH, p[0], p[1])
+        dy = -ln10 * y * (1.0 - y)                    # d y / d(n (pKa - pH))
+        J = np.stack([dy * p[1], dy * (p[0] - pH)], 1)
+        if not hill:
+            J = J[:, :1]
+        A = J.T @ J
+        g = J.T @ r
+        step = np.linalg.solve(A + mu * np.diag(np.diag(A) + 1e-30), -g)
+        trial = p.copy()
+        trial[: len(step)] += step
+        rt = resid(trial)
+        if rt @ rt < r @ r:
+            p, r = trial, rt
+            mu = max(mu * 0.3, 1e-12)
+            if np.max(np.abs(step)) < 1e-13:
+                break
+        else:
+            mu *= 10.0
+            if mu > 1e12:
+                break
+    return (float(p[0]), float(p[1])) if hill else float(p[0])
+
+
+def bootstrap(pH_levels, fractions, B=5000, seed=0, hill=False):
+    """fractions [n_pH, R]: resample R replica fractions per pH with replacement, refit,
+    95% percentile interval."""
+    f = np.asarray(fractions, np.float64)
+    npH, R = f.shape
+    pHs = np.repeat(np.asarray(pH_levels, np.float64), R)
+    est = fit_curve(pHs, f.reshape(-1), hill)
+    rng = np.random.default_rng(seed)
+    draws = []
+    for _ in range(B):
+        idx = rng.integers(0, R, size=(npH, R))
+        try:
+            draws.append(fit_curve(pHs, np.take_along_axis(f, idx, 1).reshape(-1), hill))
+        except (ValueError, np.linalg.LinAlgError):
+            continue
+    d = np.asarray(draws)
+    return est, np.percentile(d, 2.5, axis=0), np.percentile(d, 97.5, axis=0)

@@ -308,26 +308,30 @@ def make_system(cfg: int, seed: int | None = None, n_target: int | None = None) 
     if n_solv % 2:
         n_solv -= 1
     n_mobile = n_solv + 2 * n_nacl + n_his
-    nside = int(np.ceil((1.35 * n_mobile) ** (1.0 / 3.0)))
-    a = L / nside
-    g = (np.arange(nside) + 0.5) * a
-    lat = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
-    keep = np.ones((nside, nside, nside), bool)
-    rad = int(np.ceil(0.24 / a)) + 1
-    offs = np.arange(-rad, rad + 1)
-    for p in fixed_xyz:
-        c = np.floor(np.mod(p, L) / a).astype(int)
-        ix = [(c[d] + offs) % nside for d in range(3)]
-        sub = np.stack(np.meshgrid(*ix, indexing="ij"), -1).reshape(-1, 3)
-        d = (sub + 0.5) * a - p
-        d -= L * np.round(d / L)
-        close = (d * d).sum(-1) < 0.24 ** 2
-        keep[sub[close, 0], sub[close, 1], sub[close, 2]] = False
-    lat = lat[keep.reshape(-1)]
-    if len(lat) < n_mobile:
-        raise RuntimeError("not enough lattice sites for mobile particles")
+    # smallest cubic lattice that still has n_mobile free sites: spacing ~ rho^-1/3, so the
+    # initial configuration has no LJ overlaps (sigma 0.2 nm vs spacing >= 0.21 nm)
+    nside = int(np.ceil(n_mobile ** (1.0 / 3.0)))
+    while True:
+        a = L / nside
+        g = (np.arange(nside) + 0.5) * a
+        lat = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+        keep = np.ones((nside, nside, nside), bool)
+        rad = int(np.ceil(0.24 / a)) + 1
+        offs = np.arange(-rad, rad + 1)
+        for p in fixed_xyz:
+            c = np.floor(np.mod(p, L) / a).astype(int)
+            ix = [(c[d] + offs) % nside for d in range(3)]
+            sub = np.stack(np.meshgrid(*ix, indexing="ij"), -1).reshape(-1, 3)
+            d = (sub + 0.5) * a - p
+            d -= L * np.round(d / L)
+            close = (d * d).sum(-1) < 0.24 ** 2
+            keep[sub[close, 0], sub[close, 1], sub[close, 2]] = False
+        lat = lat[keep.reshape(-1)]
+        if len(lat) >= n_mobile:
+            break
+        nside += 1
     sel = rng.choice(len(lat), size=n_mobile, replace=False)
-    sites = lat[sel] + rng.uniform(-0.02, 0.02, (n_mobile, 3))
+    sites = lat[sel] + rng.uniform(-0.01, 0.01, (n_mobile, 3))
     kinds = ([("Na", 22.99, 1.0, T_NA)] * n_nacl + [("Cl", 35.45, -1.0, T_CL)] * (n_nacl + n_his))
     solv_q = np.array([0.2] * (n_solv // 2) + [-0.2] * (n_solv // 2))
     rng.shuffle(solv_q)

@@ -116,15 +116,22 @@ def test_short_horizon_trajectory(cph):
 
 
 def test_energy_conservation_without_friction(cph):
+    """gamma = 0: velocity Verlet conserves the extended-Hamiltonian energy (atoms + lambda)
+    once the lattice start has relaxed (equilibrated first with strong friction)."""
     s = make_system(1)
-    ctx = cph.cph_create(s, [4.4], [7], lambda0=np.array([[0.3]]), vel_replicas=make_velocities(s, 7)[None],
+    eq = cph.cph_create(s, [4.4], [7], lambda0=np.array([[0.3]]), vel_replicas=make_velocities(s, 7)[None],
+                        gamma_atom=10.0)
+    eq.cph_step(500)
+    x, v = eq.cph_get_positions(0)
+    lam, _ = eq.cph_get_lambdas(0)
+    ctx = cph.cph_create(s, [4.4], [7], lambda0=lam[None], pos_replicas=x[None], vel_replicas=v[None],
                          gamma_atom=0.0, gamma_lambda=0.0, nstenergy=1)
     e0 = ctx.cph_get_energies(0)
     drift = []
     for _ in range(20):
         ctx.cph_step(10)
         drift.append(ctx.cph_get_energies(0)["total"] - e0["total"])
-    print("drift", drift, "KE", e0["KE_atoms"])
+    print("drift", np.round(drift, 3), "KE", e0["KE_atoms"])
     assert np.max(np.abs(drift)) < 2e-3 * e0["KE_atoms"]
 
 
