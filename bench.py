@@ -58,7 +58,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                          "-lms", "50", "-i", str(self.device)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -170,8 +170,8 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="cph", choices=["cph", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--replicas", type=int, default=0)
@@ -198,7 +198,10 @@ def main():
     pH = np.resize(np.asarray(s.pH_grid, np.float64), R)
     seeds = replica_seeds(cfg, R, base=rank)
     vel = np.stack([make_velocities(s, 1000 * rank + r) for r in range(R)])
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) torch stream: the library launches on it and the CUDA
+    # events below are recorded on it
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     ctx = cph.cph_create(s, pH, seeds, vel_replicas=vel, device=local, cuda_stream=stream.cuda_stream)
     W = max(args.warmup, 3)
     K = args.steps

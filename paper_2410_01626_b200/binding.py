@@ -127,7 +127,10 @@ def _torch_allocator(device):
         return torch.cuda.caching_allocator_alloc(int(nbytes), device=device)
 
     def free(ptr, _ctx):
-        torch.cuda.caching_allocator_delete(ptr)
+        try:
+            torch.cuda.caching_allocator_delete(ptr)
+        except Exception:          # interpreter shutdown: torch may already be torn down
+            pass
     return ALLOC_FN(alloc), FREE_FN(free)
 
 
@@ -206,6 +209,8 @@ def cph_create(system, pH, replica_seed, *, lambda0=None, pos_replicas=None, vel
                 cbs = _torch_allocator(device)
                 p.dev_alloc, p.dev_free = cbs
                 if cuda_stream is None:
+                    # torch's legacy default stream has handle 0; the library then uses its own
+                    # stream (graph capture is not allowed on the legacy stream)
                     p.cuda_stream = torch.cuda.current_stream(device).cuda_stream or None
         except ImportError:
             cbs = None

@@ -20,6 +20,14 @@ constexpr double kLn10 = 2.30258509299404568402;
 constexpr int kNE = CPH_N_ETERMS;
 constexpr int kMaxTypes = 32;                // LJ table kept in shared memory
 
+// neighbour-list entry: sorted slot j (21 bits) | LJ type of j (5 bits) | image code (5 bits)
+// image code = (kx+1)*9 + (ky+1)*3 + (kz+1), k = rint((x_j - x_i)/L) at the rebuild
+constexpr uint32_t kEntryJMask = 0x1FFFFFu;
+constexpr int kEntryTypeShift = 21;
+constexpr uint32_t kEntryTypeMask = 0x1Fu;
+constexpr int kEntryImgShift = 26;
+constexpr int kMaxAtoms = 1 << 21;
+
 // Device-side flags (int array)
 enum { FLAG_PENDING_CLOSE = 0, FLAG_LIST_OVERFLOW = 1, FLAG_DIVERGED = 2, FLAG_MAX_NNB = 3,
        FLAG_STEP_DONE = 4, FLAG_COUNT = 8 };
@@ -94,6 +102,7 @@ struct DevBufs {
   int *flags = nullptr;
   uint64_t *seed = nullptr;                         // [R]
   double *phi_lam = nullptr;                        // [R*nlam] total phi of lambda atoms
+  int *k_group = nullptr;                           // [nlam] group of each lambda atom
 };
 
 struct Ctx {

@@ -267,7 +267,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   auto bad = [&](const char *m) { c.err = m; return fail_create(ctx, CPH_E_INVALID); };
   if (prm->abi_version != CPH_ABI_VERSION) return bad("abi_version mismatch");
   const int N = sys->n_atoms, R = prm->n_replicas, G = sys->n_groups, T = sys->n_types;
-  if (N < 1 || N >= (1 << 24)) return bad("n_atoms must be in [1, 2^24)");
+  if (N < 1 || N > kMaxAtoms) return bad("n_atoms must be in [1, 2^21]");
   if (R < 1) return bad("n_replicas must be >= 1");
   if (!sys->pos || !sys->mass || !sys->charge || !sys->type || !sys->c6 || !sys->c12)
     return bad("system arrays pos/mass/charge/type/c6/c12 are required");
@@ -357,6 +357,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     c.h_pKa.assign(sys->pKa, sys->pKa + 3 * (size_t)G);
   }
   const int C = c.h_cptr[G];
+  if (nlam > 12000) { c.err = "more than 12000 lambda atoms per replica"; return fail_create(ctx, CPH_E_UNSUPPORTED); }
   if (prm->lambda0 && !finite_arr(prm->lambda0, (size_t)R * C)) return bad("non-finite lambda0");
 
   // ---- kernel parameters ------------------------------------------------------------
@@ -469,6 +470,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   d.g_kind = dalloc<int>(c, G); d.g_ptr = dalloc<int>(c, G + 1);
   d.g_atoms = dalloc<int>(c, nlam); d.g_cptr = dalloc<int>(c, G + 1);
   d.g_q = dalloc<double>(c, 4 * (size_t)nlam);
+  d.k_group = dalloc<int>(c, nlam);
   d.vmm = dalloc<double>(c, 36 * (size_t)G);
   d.g_dG = dalloc<double>(c, (size_t)R * G * 3);
   d.d1 = dalloc<double>(c, (size_t)R * C);
@@ -532,6 +534,10 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
         UP(d.g_kind, c.h_group_kind.data(), G); UP(d.g_ptr, c.h_group_ptr.data(), G + 1);
         UP(d.g_atoms, c.h_group_atoms.data(), nlam); UP(d.g_cptr, c.h_cptr.data(), G + 1);
         UP(d.g_q, c.h_state_q.data(), 4 * (size_t)nlam); UP(d.vmm, sys->vmm, 36 * (size_t)G);
+        std::vector<int> kg(nlam);
+        for (int g = 0; g < G; ++g)
+          for (int k = c.h_group_ptr[g]; k < c.h_group_ptr[g + 1]; ++k) kg[k] = g;
+        UP(d.k_group, kg.data(), nlam);
       }
       if (C) UP(d.lam, lam0.data(), (size_t)R * C);
       UP(d.seed, c.h_seed.data(), R);
@@ -784,7 +790,7 @@ cph_status cph_get_pairlist(cph_ctx *ctx, int32_t r, int32_t *pairs, int64_t cap
   for (size_t i = 0; i < N; ++i) {
     const int oi = meta[i].x;
     for (int k = 0; k < std::min(nnb[i], kp.cap); ++k) {
-      const int j = (int)(nbl[(size_t)k * kp.Nst + i] & 0xFFFFFFu);
+      const int j = (int)(nbl[(size_t)k * kp.Nst + i] & kEntryJMask);
       const int oj = meta[j].x;
       if (oi < oj) out.emplace_back(oi, oj);
     }

@@ -74,18 +74,17 @@ __global__ void __launch_bounds__(128) k_close(KParams kp, DevBufs d, int kick) 
 // ---- lambda helpers ---------------------------------------------------------------------
 // charges of every lambda atom of replica r from its group's (lp, lt) (Eq. 2)
 __device__ void lambda_set_charges(const KParams &kp, const DevBufs &d, int r) {
-  for (int g = threadIdx.x; g < kp.G; g += blockDim.x) {
+  for (int k = threadIdx.x; k < kp.nlam; k += blockDim.x) {       // one thread per lambda atom
+    const int g = d.k_group[k];
     const int c0 = d.g_cptr[g];
     const double lp = d.lam[(size_t)r * kp.C + c0];
     const double lt = d.g_kind[g] == 3 ? d.lam[(size_t)r * kp.C + c0 + 1] : 0.0;
     const double wA = (1.0 - lp) * (1.0 - lt), wB = (1.0 - lp) * lt, wC = lp * (1.0 - lt), wD = lp * lt;
-    for (int k = d.g_ptr[g]; k < d.g_ptr[g + 1]; ++k) {
-      const double *qs = d.g_q + 4 * (size_t)k;
-      const double q = wA * qs[0] + wB * qs[1] + wC * qs[2] + wD * qs[3];
-      d.qlam[(size_t)r * kp.nlam + k] = q;
-      const int slot = d.iperm[(size_t)r * kp.N + d.g_atoms[k]];
-      d.xyzq[(size_t)r * kp.Nst + slot].w = (float)q;
-    }
+    const double *qs = d.g_q + 4 * (size_t)k;
+    const double q = wA * qs[0] + wB * qs[1] + wC * qs[2] + wD * qs[3];
+    d.qlam[(size_t)r * kp.nlam + k] = q;
+    const int slot = d.iperm[(size_t)r * kp.N + d.g_atoms[k]];
+    d.xyzq[(size_t)r * kp.Nst + slot].w = (float)q;
   }
 }
 
@@ -148,15 +147,25 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
   }
   const double Q = kp.Q_fixed + block_sum_d(qs);
   const double Q2 = kp.Q2_fixed + block_sum_d(qq);
-  // full potential of each lambda atom (real + excl + recip + self + net)
+  // per lambda atom (one thread each): full potential (real + excl + recip + self + net) and
+  // its products with dq/dlp, dq/dlt, staged in shared memory for the per-group sums
+  extern __shared__ double s_dq[];            // [2 * nlam]
   for (int k = threadIdx.x; k < kp.nlam; k += blockDim.x) {
     const size_t ix = (size_t)r * kp.nlam + k;
     const double q = d.qlam[ix];
-    d.phi_lam[ix] = d.phi64_nb[ix] + d.phi64_rec[ix] - 2.0 * kp.beta_d / sqrtpi * q -
-                    kPi * Q / (V * kp.beta_d * kp.beta_d);
+    const double phi = d.phi64_nb[ix] + d.phi64_rec[ix] - 2.0 * kp.beta_d / sqrtpi * q -
+                       kPi * Q / (V * kp.beta_d * kp.beta_d);
+    d.phi_lam[ix] = phi;
+    const int g = d.k_group[k];
+    const size_t ic = (size_t)r * kp.C + d.g_cptr[g];
+    const double lp = d.lam[ic];
+    const double lt = d.g_kind[g] == 3 ? d.lam[ic + 1] : 0.0;
+    const double *q4 = d.g_q + 4 * (size_t)k;
+    s_dq[2 * k] = ((1.0 - lt) * (q4[2] - q4[0]) + lt * (q4[3] - q4[1])) * phi;
+    s_dq[2 * k + 1] = ((1.0 - lp) * (q4[1] - q4[0]) + lp * (q4[3] - q4[2])) * phi;
   }
   __syncthreads();
-  // per group: Coulomb dV/dlambda and bias
+  // per group: Coulomb dV/dlambda (fixed-order sum over the group's atoms) and bias
   double ebias = 0.0;
   for (int g = threadIdx.x; g < kp.G; g += blockDim.x) {
     const int kind = d.g_kind[g];
@@ -166,10 +175,8 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
     const double lt = kind == 3 ? d.lam[ic + 1] : 0.0;
     double sp = 0.0, st = 0.0;
     for (int k = d.g_ptr[g]; k < d.g_ptr[g + 1]; ++k) {
-      const double *q4 = d.g_q + 4 * (size_t)k;
-      const double phi = d.phi_lam[(size_t)r * kp.nlam + k];
-      sp += ((1.0 - lt) * (q4[2] - q4[0]) + lt * (q4[3] - q4[1])) * phi;
-      st += ((1.0 - lp) * (q4[1] - q4[0]) + lp * (q4[3] - q4[2])) * phi;
+      sp += s_dq[2 * k];
+      st += s_dq[2 * k + 1];
     }
     // bias (Eq. 3): Vmm + VpH + Vdw
     double vm, vmp, vmt;
@@ -265,7 +272,13 @@ int launch_close(Ctx &c, cudaStream_t s, int kick) {
   return 1;
 }
 int launch_lambda_reduce(Ctx &c, cudaStream_t s, int mode) {
-  k_lambda_reduce<<<c.kp.R, 256, 0, s>>>(c.kp, c.d, mode);
+  const size_t smem = 2 * sizeof(double) * (size_t)c.kp.nlam;
+  static size_t configured = 48 * 1024;
+  if (smem > configured) {
+    cudaFuncSetAttribute(k_lambda_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  k_lambda_reduce<<<c.kp.R, 256, 2 * sizeof(double) * (size_t)c.kp.nlam, s>>>(c.kp, c.d, mode);
   return 1;
 }
 int launch_lambda_open(Ctx &c, cudaStream_t s) {

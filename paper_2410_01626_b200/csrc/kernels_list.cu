@@ -101,7 +101,12 @@ __global__ void k_permute(KParams kp, DevBufs d) {
   const size_t base = (size_t)r * kp.Nst;
   const int old = d.perm_tmp[base + i];
   const int2 m = d.meta[base + old];
-  d.xyzq_alt[base + i] = d.xyzq[base + old];
+  // wrap into the home box: list entries then carry each pair's image (kEntryImgShift)
+  float4 x = d.xyzq[base + old];
+  x.x -= kp.L[0] * floorf(x.x * kp.invL[0]);
+  x.y -= kp.L[1] * floorf(x.y * kp.invL[1]);
+  x.z -= kp.L[2] * floorf(x.z * kp.invL[2]);
+  d.xyzq_alt[base + i] = x;
   d.vel_alt[base + i] = d.vel[base + old];
   d.meta_alt[base + i] = m;
   d.iperm[(size_t)r * kp.N + m.x] = i;
@@ -116,52 +121,80 @@ __global__ void k_copy_back(KParams kp, DevBufs d) {
   d.meta[idx] = d.meta_alt[idx];
 }
 
-__global__ void __launch_bounds__(128) k_build_list(KParams kp, DevBufs d) {
-  const int r = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= kp.N) return;
+// One warp per cell: the i atoms are the cell's atoms (one per lane, chunks of 32), and every
+// stencil cell's atoms are staged through shared memory (coalesced loads, broadcast reads),
+// so the loop structure is uniform across the warp.
+__global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
+  const int r = blockIdx.y, c = blockIdx.x;
+  const int lane = threadIdx.x;
   const size_t base = (size_t)r * kp.Nst;
   const float4 *xq = d.xyzq + base;
   const int2 *meta = d.meta + base;
   const int *start = d.cell_start + (size_t)r * (kp.ncell + 1);
-  const float4 xi = xq[i];
-  const int orig = meta[i].x;
-  const int eb = d.excl_ptr[orig], ee = d.excl_ptr[orig + 1];
-  const int cx = cell_coord(xi.x, kp.invL[0], kp.nc[0]);
-  const int cy = cell_coord(xi.y, kp.invL[1], kp.nc[1]);
-  const int cz = cell_coord(xi.z, kp.invL[2], kp.nc[2]);
-  uint32_t *out = d.nbl + (size_t)r * kp.cap * kp.Nst + i;
-  int cnt = 0;
-  for (int ox = 0; ox < kp.ns[0]; ++ox) {
-    const int gx = (cx + kp.so[0] + ox + 2 * kp.nc[0]) % kp.nc[0];
-    for (int oy = 0; oy < kp.ns[1]; ++oy) {
-      const int gy = (cy + kp.so[1] + oy + 2 * kp.nc[1]) % kp.nc[1];
-      for (int oz = 0; oz < kp.ns[2]; ++oz) {
-        const int gz = (cz + kp.so[2] + oz + 2 * kp.nc[2]) % kp.nc[2];
-        const int c = (gx * kp.nc[1] + gy) * kp.nc[2] + gz;
-        const int jb = start[c], je = start[c + 1];
-        for (int j = jb; j < je; ++j) {
-          if (j == i) continue;
-          const float4 xj = xq[j];
-          // canonical formula (R14): dx = x_j - x_i ; dx -= L rint(dx / L)
-          const float dx = min_image_rn(__fsub_rn(xj.x, xi.x), kp.L[0], kp.invL[0]);
-          const float dy = min_image_rn(__fsub_rn(xj.y, xi.y), kp.L[1], kp.invL[1]);
-          const float dz = min_image_rn(__fsub_rn(xj.z, xi.z), kp.L[2], kp.invL[2]);
-          const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-          if (!(d2 < kp.rlist2)) continue;
-          const int2 mj = meta[j];
-          bool ex = false;
-          for (int e = eb; e < ee; ++e) ex |= (d.excl_idx[e] == mj.x);
-          if (ex) continue;
-          if (cnt < kp.cap) out[(size_t)cnt * kp.Nst] = (uint32_t)j | ((uint32_t)(mj.y & 0xFF) << 24);
-          ++cnt;
+  __shared__ float4 sx[32];
+  __shared__ int sj[32];
+  const int cz = c % kp.nc[2], cy = (c / kp.nc[2]) % kp.nc[1], cx = c / (kp.nc[2] * kp.nc[1]);
+  const int ib = start[c], ie = start[c + 1];
+  for (int i0 = ib; i0 < ie; i0 += 32) {
+    const int i = i0 + lane;
+    const bool valid = i < ie;
+    const float4 xi = valid ? xq[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int orig = valid ? meta[i].x : 0;
+    const int eb = valid ? d.excl_ptr[orig] : 0, ee = valid ? d.excl_ptr[orig + 1] : 0;
+    uint32_t *out = d.nbl + (size_t)r * kp.cap * kp.Nst + (valid ? i : 0);
+    int cnt = 0;
+    for (int ox = 0; ox < kp.ns[0]; ++ox) {
+      const int gx = (cx + kp.so[0] + ox + 2 * kp.nc[0]) % kp.nc[0];
+      for (int oy = 0; oy < kp.ns[1]; ++oy) {
+        const int gy = (cy + kp.so[1] + oy + 2 * kp.nc[1]) % kp.nc[1];
+        for (int oz = 0; oz < kp.ns[2]; ++oz) {
+          const int gz = (cz + kp.so[2] + oz + 2 * kp.nc[2]) % kp.nc[2];
+          const int cc = (gx * kp.nc[1] + gy) * kp.nc[2] + gz;
+          const int jb = start[cc], je = start[cc + 1];
+          for (int j0 = jb; j0 < je; j0 += 32) {
+            const int nj = min(32, je - j0);
+            __syncwarp();
+            if (lane < nj) {
+              const int j = j0 + lane;
+              sx[lane] = xq[j];
+              sj[lane] = j | ((meta[j].y & (int)kEntryTypeMask) << kEntryTypeShift);
+            }
+            __syncwarp();
+            if (!valid) continue;
+            for (int t = 0; t < nj; ++t) {
+              const float4 xj = sx[t];
+              // canonical formula (R14): dx = x_j - x_i ; dx -= L rint(dx / L)
+              const float rx = __fsub_rn(xj.x, xi.x), ry = __fsub_rn(xj.y, xi.y), rz = __fsub_rn(xj.z, xi.z);
+              const float kx = rintf(__fmul_rn(rx, kp.invL[0]));
+              const float ky = rintf(__fmul_rn(ry, kp.invL[1]));
+              const float kz = rintf(__fmul_rn(rz, kp.invL[2]));
+              const float dx = __fsub_rn(rx, __fmul_rn(kp.L[0], kx));
+              const float dy = __fsub_rn(ry, __fmul_rn(kp.L[1], ky));
+              const float dz = __fsub_rn(rz, __fmul_rn(kp.L[2], kz));
+              const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+              const int je_ = sj[t] | ((((int)kx + 1) * 9 + ((int)ky + 1) * 3 + ((int)kz + 1)) << kEntryImgShift);
+              const int j = je_ & (int)kEntryJMask;
+              if (!(d2 < kp.rlist2) || j == i) continue;
+              if (ee > eb) {
+                const int oj = meta[j].x;
+                bool ex = false;
+                for (int e = eb; e < ee; ++e) ex |= (d.excl_idx[e] == oj);
+                if (ex) continue;
+              }
+              if (cnt < kp.cap) out[(size_t)cnt * kp.Nst] = (uint32_t)je_;
+              ++cnt;
+            }
+          }
         }
       }
     }
-  }
-  d.nnb[base + i] = cnt;
-  if (cnt > kp.cap) {
-    d.flags[FLAG_LIST_OVERFLOW] = 1;
-    atomicMax(&d.flags[FLAG_MAX_NNB], cnt);
+    if (valid) {
+      d.nnb[base + i] = cnt;
+      if (cnt > kp.cap) {
+        d.flags[FLAG_LIST_OVERFLOW] = 1;
+        atomicMax(&d.flags[FLAG_MAX_NNB], cnt);
+      }
+    }
   }
 }
 
@@ -175,7 +208,7 @@ int launch_rebuild(Ctx &c, cudaStream_t s) {
   k_cell_sort<<<dim3((kp.ncell + 127) / 128, kp.R), 128, 0, s>>>(kp, c.d);
   k_permute<<<ga, 128, 0, s>>>(kp, c.d);
   k_copy_back<<<ga, 128, 0, s>>>(kp, c.d);
-  k_build_list<<<ga, 128, 0, s>>>(kp, c.d);
+  k_build_list<<<dim3(kp.ncell, kp.R), 32, 0, s>>>(kp, c.d);
   return 7;
 }
 

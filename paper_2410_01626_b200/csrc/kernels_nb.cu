@@ -7,64 +7,86 @@
 //   phi_i += q_j erfc(beta r)/r
 //   F_i   += [f q_i q_j (erfc(beta r)/r + 2 beta/sqrt(pi) e^{-beta^2 r^2}) + 12 c12/r^12 - 6 c6/r^6] / r^2 * (x_i - x_j)
 // Excluded pairs (any distance) get the erf correction -f q_i q_j erf(beta r)/r.
-// Warps that contain a lambda atom accumulate phi in fp64 as well (dV/dlambda needs it at
-// the 2e-5 level; BASELINE "fp64 lambda reductions").  Energies are evaluated on energy
-// steps only (E_real = 1/2 f sum_i q_i phi_i, so only LJ needs a per-pair energy).
+// List entries carry the periodic image of j fixed at the last rebuild (positions are
+// wrapped into the box then), so no per-pair minimum-image arithmetic is needed.
+// Warps that contain a lambda atom also accumulate phi in fp64 (dV/dlambda at 2e-5; BASELINE
+// "fp64 lambda reductions"); on energy steps the per-atom sums are fp64 as well.
+// Compiled with -ftz=true: no denormal fix-ups around MUFU.RSQ / RCP / EX2.
 #include "cph_device.cuh"
 
 namespace cph {
 
 template <bool ENERGY, bool PHI64>
 __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, const float4 *__restrict__ xq,
-                                        const float4 *__restrict__ lj, int r, int i, bool valid,
+                                        const float2 *__restrict__ ljf, const float2 *__restrict__ lje,
+                                        const float4 *__restrict__ shift, int r, int i, bool valid,
                                         float4 xi, int ti, int lslot, int n, int nmax,
                                         double *e_lj, double *e_real, double *e_excl) {
   const float qif = kp.fcoul * xi.w;
-  float fx = 0.f, fy = 0.f, fz = 0.f, phi = 0.f, elj = 0.f;
-  double phid = 0.0;
+  float fx = 0.f, fy = 0.f, fz = 0.f, phi = 0.f;
+  double phid = 0.0, elj = 0.0;        // fp64 only in lambda warps / on energy steps
   const uint32_t *L = d.nbl + (size_t)r * kp.cap * kp.Nst + i;
-  const float4 *ljrow = lj + ti * kp.T;
-  const float Lx = kp.L[0], Ly = kp.L[1], Lz = kp.L[2];
-  const float iLx = kp.invL[0], iLy = kp.invL[1], iLz = kp.invL[2];
+  const float2 *ljrow = ljf + ti * kp.T;
+  const float2 *ljerow = lje + ti * kp.T;
   const float rc2 = kp.rc2, beta = kp.beta, c2b = kp.two_beta_sqrtpi;
-  const float nlog2e = -1.4426950408889634f;
-#pragma unroll 2
-  for (int k = 0; k < nmax; ++k) {
-    if (k < n) {
-      const uint32_t e = __ldcs(L + (size_t)k * kp.Nst);
-      const int j = (int)(e & 0xFFFFFFu);
-      const int tj = (int)(e >> 24);
-      const float4 xj = __ldg(xq + j);
-      float dx = xi.x - xj.x, dy = xi.y - xj.y, dz = xi.z - xj.z;
-      dx -= Lx * rintf(dx * iLx);
-      dy -= Ly * rintf(dy * iLy);
-      dz -= Lz * rintf(dz * iLz);
+  const float kexp = -kp.beta * kp.beta * 1.4426950408889634f;   // exp(-b^2 r^2) = 2^(kexp r^2)
+  const float pbeta = kErfcP * kp.beta;
+  constexpr int U = 4;                 // neighbours in flight per lane
+  // Entries past a lane's own count point at the lane's own atom with zero shift (r2 = 0,
+  // masked), so a chunk's U loads are unconditional and the next chunk's entries are
+  // prefetched while the current chunk computes.
+  const uint32_t self = (uint32_t)(valid ? i : 0) | ((uint32_t)ti << kEntryTypeShift) |
+                        (13u << kEntryImgShift);
+  uint32_t en[U];
+  const int stride = kp.Nst;
+#pragma unroll
+  for (int u = 0; u < U; ++u) en[u] = u < n ? __ldcs(L + u * stride) : self;
+  const uint32_t *Lk = L + U * stride;
+  for (int k0 = 0; k0 < nmax; k0 += U, Lk += U * stride) {
+    uint32_t e[U];
+    float4 xj[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      e[u] = en[u];
+      xj[u] = __ldg(&xq[(int)(e[u] & kEntryJMask)]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) en[u] = k0 + U + u < n ? __ldcs(Lk + u * stride) : self;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float4 sh = shift[e[u] >> kEntryImgShift];
+      const float dx = (xi.x - xj[u].x) + sh.x;
+      const float dy = (xi.y - xj[u].y) + sh.y;
+      const float dz = (xi.z - xj[u].z) + sh.z;
       const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      const bool in = r2 < rc2;
+      const bool in = (r2 < rc2) && (r2 > 0.0f);
       const float rinv = rsqrtf(r2);
       const float r2inv = rinv * rinv;
-      const float4 c = ljrow[tj];                       // (6 c6, 12 c12, c6, c12)
+      const float2 c = ljrow[(e[u] >> kEntryTypeShift) & kEntryTypeMask];   // (6 c6, 12 c12)
       const float r6 = r2inv * r2inv * r2inv;
       const float flj = r6 * fmaf(c.y, r6, -c.x);
-      const float z = beta * (r2 * rinv);
-      const float t = __fdividef(1.0f, fmaf(kErfcP, z, 1.0f));
-      const float ez = exp2f(z * z * nlog2e);
-      const float erfc_r = erfc_poly(t) * ez * rinv;
-      const float qj = xj.w;
-      const float qe = in ? qj * erfc_r : 0.f;
-      const float fs = in ? fmaf(qif, fmaf(qj * c2b, ez, qe), flj) * r2inv : 0.f;
+      const float t = __fdividef(1.0f, fmaf(pbeta, r2 * rinv, 1.0f));   // 1/(1 + p beta r)
+      const float ez = exp2f(r2 * kexp);                                 // exp(-beta^2 r^2)
+      const float bq = xj[u].w * ez;                                     // q_j e^{-z^2}
+      const float qe = in ? erfc_poly(t) * bq * rinv : 0.f;              // q_j erfc(beta r)/r
+      const float fs = in ? fmaf(qif, fmaf(c2b, bq, qe), flj) * r2inv : 0.f;
       phi += qe;
       fx = fmaf(fs, dx, fx);
       fy = fmaf(fs, dy, fy);
       fz = fmaf(fs, dz, fz);
-      if (PHI64) phid += (double)qe;
-      if (ENERGY) elj += in ? r6 * fmaf(c.w, r6, -c.z) : 0.f;
+      if (PHI64 || ENERGY) phid += (double)qe;
+      if (ENERGY) {
+        const float2 ce = ljerow[(e[u] >> kEntryTypeShift) & kEntryTypeMask];   // (c6, c12)
+        elj += in ? (double)(r6 * fmaf(ce.y, r6, -ce.x)) : 0.0;
+      }
     }
   }
   // exclusion corrections (solute atoms only; most atoms have none)
   float phx = 0.f;
   double phxd = 0.0;
   if (valid) {
+    const float Lx = kp.L[0], Ly = kp.L[1], Lz = kp.L[2];
+    const float iLx = kp.invL[0], iLy = kp.invL[1], iLz = kp.invL[2];
     const int orig = d.meta[(size_t)r * kp.Nst + i].x;
     const int eb = d.excl_ptr[orig], ee = d.excl_ptr[orig + 1];
     for (int e = eb; e < ee; ++e) {
@@ -78,11 +100,11 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
       const float rinv = rsqrtf(r2);
       const float z = beta * (r2 * rinv);
       const float t = __fdividef(1.0f, fmaf(kErfcP, z, 1.0f));
-      const float ez = exp2f(z * z * nlog2e);
+      const float ez = exp2f(r2 * kexp);
       const float erf_r = rinv - erfc_poly(t) * ez * rinv;   // erf(beta r)/r
       const float qj = xj.w;
       phx -= qj * erf_r;
-      if (PHI64) phxd -= (double)(qj * erf_r);
+      if (PHI64 || ENERGY) phxd -= (double)(qj * erf_r);
       const float fs = qif * qj * (c2b * ez - erf_r) * rinv * rinv;
       fx = fmaf(fs, dx, fx);
       fy = fmaf(fs, dy, fy);
@@ -93,17 +115,25 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
     if (PHI64 && lslot >= 0) d.phi64_nb[(size_t)r * kp.nlam + lslot] = phid + phxd;
   }
   if (ENERGY && valid) {
-    *e_lj = 0.5 * (double)elj;
-    *e_real = 0.5 * (double)qif * (double)phi;
-    *e_excl = 0.5 * (double)qif * (double)phx;
+    *e_lj = 0.5 * elj;
+    *e_real = 0.5 * (double)kp.fcoul * (double)xi.w * phid;
+    *e_excl = 0.5 * (double)kp.fcoul * (double)xi.w * phxd;
   }
 }
 
 __global__ void __launch_bounds__(128) k_nonbonded(KParams kp, DevBufs d, int step_offset) {
-  __shared__ float4 s_lj[kMaxTypes * kMaxTypes];
+  __shared__ float2 s_ljf[kMaxTypes * kMaxTypes];   // (6 c6, 12 c12) for forces
+  __shared__ float2 s_lje[kMaxTypes * kMaxTypes];   // (c6, c12) for energies
+  __shared__ float4 s_shift[27];                    // image shift L * (kx, ky, kz)
   for (int t = threadIdx.x; t < kp.T * kp.T; t += blockDim.x) {
-    const float2 c = d.ljtab[t];                // (6 c6, 12 c12)
-    s_lj[t] = make_float4(c.x, c.y, c.x / 6.0f, c.y / 12.0f);
+    const float2 c = d.ljtab[t];
+    s_ljf[t] = c;
+    s_lje[t] = make_float2(c.x / 6.0f, c.y / 12.0f);
+  }
+  if (threadIdx.x < 27) {
+    const int code = threadIdx.x;
+    s_shift[code] = make_float4(kp.L[0] * (float)(code / 9 - 1), kp.L[1] * (float)((code / 3) % 3 - 1),
+                                kp.L[2] * (float)(code % 3 - 1), 0.f);
   }
   __syncthreads();
   const int r = blockIdx.y;
@@ -122,11 +152,11 @@ __global__ void __launch_bounds__(128) k_nonbonded(KParams kp, DevBufs d, int st
   const float4 *xq = d.xyzq + (size_t)r * kp.Nst;
   double elj = 0.0, ere = 0.0, eex = 0.0;
   if (warp_lam) {
-    if (energy) nb_atom<true, true>(kp, d, xq, s_lj, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
-    else nb_atom<false, true>(kp, d, xq, s_lj, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
+    if (energy) nb_atom<true, true>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
+    else nb_atom<false, true>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
   } else {
-    if (energy) nb_atom<true, false>(kp, d, xq, s_lj, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
-    else nb_atom<false, false>(kp, d, xq, s_lj, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
+    if (energy) nb_atom<true, false>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
+    else nb_atom<false, false>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
   }
   if (energy) {
     double *e = d.erec + ((size_t)(m & 1) * kp.R + r) * kNE;
