@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -207,7 +208,8 @@ cph_status capture_block(Ctx &c) {
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
   int k = 0;
-  for (int s = 0; s < c.kp.nstlist; ++s) k += enqueue_step(c, s == c.kp.nstlist - 1, true);
+  const bool two = getenv("CPH_ONE_STREAM") == nullptr;   // diagnostic switch: serialise NB and PME
+  for (int s = 0; s < c.kp.nstlist; ++s) k += enqueue_step(c, s == c.kp.nstlist - 1, two);
   CK(cudaStreamEndCapture(c.stream, &g));
   CK(cudaGraphInstantiate(&c.graph_block, g, 0));
   cudaGraphDestroy(g);
@@ -630,7 +632,7 @@ cph_status cph_step(cph_ctx *ctx, int64_t n_steps) {
       k += c.graph_block_kernels;
       c.host_step += nl;
     } else {
-      k += enqueue_step(c, (c.host_step + 1) % nl == 0, true);
+      k += enqueue_step(c, (c.host_step + 1) % nl == 0, getenv("CPH_ONE_STREAM") == nullptr);
       c.host_step += 1;
     }
   }

@@ -143,8 +143,9 @@ def test_replicas_independent_and_deterministic(cph):
     b, *_ = _ctx(cph, s, 3, seed=3)
     a.cph_step(25)
     b.cph_step(25)
+    # fp32 atomics in the PME spread make runs reproducible to rounding, not bitwise
     for r in range(3):
-        np.testing.assert_array_equal(a.cph_get_lambdas(r)[0], b.cph_get_lambdas(r)[0])
+        np.testing.assert_allclose(a.cph_get_lambdas(r)[0], b.cph_get_lambdas(r)[0], atol=1e-6)
     # replica 1 alone (R=1) gives the same lambda trajectory as inside the batch, up to fp32
     # atomics ordering in the PME spread
     ctx1 = cph.cph_create(s, [np.linspace(3, 7, 3)[1]], [replica_seeds(99, 3, 3)[1]],
