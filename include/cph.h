@@ -78,7 +78,7 @@ enum {
 };
 
 typedef struct {
-  int32_t n_atoms;              /* N >= 1, N <= 2^24 */
+  int32_t n_atoms;              /* N >= 1, N <= 2^21 */
   const float *pos;             /* [N*3] nm, any image */
   const float *vel;             /* [N*3] nm/ps or NULL (zero) */
   const float *mass;            /* [N] u; 0 = frozen (never moved) */

@@ -20,22 +20,17 @@ constexpr double kLn10 = 2.30258509299404568402;
 constexpr int kNE = CPH_N_ETERMS;
 constexpr int kMaxTypes = 32;                // LJ table kept in shared memory
 
-// neighbour-list entry: region-local index of j (16 bits) | LJ type of j (5 bits) | image
-// code (5 bits); image code = (kx+1)*9 + (ky+1)*3 + (kz+1), k = rint((x_j - x_i)/L) at the
-// rebuild.  The region is the shared-memory copy of the atoms of cells within +-2 cells of
-// the block that owns atom i (see region.cuh).
-constexpr uint32_t kEntryJMask = 0xFFFFu;
-constexpr int kEntryTypeShift = 16;
+// neighbour-list entry: sorted slot j (21 bits) | LJ type of j (5 bits) | image code (5 bits)
+// image code = (kx+1)*9 + (ky+1)*3 + (kz+1), k = rint((x_j - x_i)/L) at the rebuild
+constexpr uint32_t kEntryJMask = 0x1FFFFFu;
+constexpr int kEntryTypeShift = 21;
 constexpr uint32_t kEntryTypeMask = 0x1Fu;
-constexpr int kEntryImgShift = 21;
-constexpr int kMaxAtoms = 1 << 24;
-constexpr int kMaxRegionAtoms = 1 << 16;
-constexpr int kMaxRegionCells = 2048;
-constexpr int kMaxBlockCells = 128;
+constexpr int kEntryImgShift = 26;
+constexpr int kMaxAtoms = 1 << 21;
 
 // Device-side flags (int array)
 enum { FLAG_PENDING_CLOSE = 0, FLAG_LIST_OVERFLOW = 1, FLAG_DIVERGED = 2, FLAG_MAX_NNB = 3,
-       FLAG_STEP_DONE = 4, FLAG_REGION_MAX = 5, FLAG_REGION_OVERFLOW = 6, FLAG_COUNT = 8 };
+       FLAG_STEP_DONE = 4, FLAG_COUNT = 8 };
 
 // Scalars every kernel needs, passed by value.
 struct KParams {
@@ -52,12 +47,6 @@ struct KParams {
   int ns[3], so[3];            // stencil sizes and first offsets per dimension
   // list
   int cap;                     // neighbour capacity per atom
-  // blocks: groups of b[d] cells; each block's region (block +- 2 cells, or the whole
-  // dimension) is staged in shared memory by the list builder and the pair kernel
-  int b[3], nb[3], nblk;       // block size in cells, blocks per dimension, blocks per replica
-  int rcap;                    // region atom capacity (shared memory slots)
-  int rcells;                  // max region cells
-  int bthreads;                // threads per block CTA
   // PME
   int K[3], K3, Kc;            // grid, K^3, complex points per replica
   int Kzc;                     // Kz/2+1
@@ -150,7 +139,6 @@ int launch_integrate(Ctx &c, cudaStream_t s, int do_open);       // BAOA (+ pend
 int launch_close(Ctx &c, cudaStream_t s, int kick);                // final half kick / KE
 int launch_rebuild(Ctx &c, cudaStream_t s);                        // sort + pair list
 int launch_nonbonded(Ctx &c, cudaStream_t s, int step_offset);
-size_t nonbonded_smem(const KParams &kp);
 int launch_spread(Ctx &c, cudaStream_t s);
 int launch_solve(Ctx &c, cudaStream_t s, int step_offset);
 int launch_gather(Ctx &c, cudaStream_t s);

@@ -104,61 +104,6 @@ bool finite_arr(const double *p, size_t n) {
   return true;
 }
 
-// Block decomposition (region.cuh): pick b[3] cells per block so that the staged region
-// (block +- 2 cells) fits comfortably in shared memory (two CTAs per SM) while the block's
-// own atoms are as large a fraction of its region as possible.
-size_t nonbonded_smem_bytes_for(const KParams &kp0, int rcap) {
-  KParams kp = kp0;
-  kp.rcap = rcap;
-  return nonbonded_smem(kp);
-}
-
-int region_width(const KParams &kp, int d, int bw) {
-  return (kp.ns[d] < 5 || bw + 4 >= kp.nc[d]) ? kp.nc[d] : bw + 4;
-}
-
-void set_region_capacity(KParams &kp, int rcap) {
-  kp.rcap = std::min(std::max(rcap, 64), kMaxRegionAtoms - 1);
-}
-
-void choose_blocks(KParams &kp, int N) {
-  const double a = (double)N / kp.ncell;        // mean atoms per cell
-  double best = -1.0;
-  int bb[3] = {1, 1, 1};
-  for (int bx = 1; bx <= std::min(kp.nc[0], 8); ++bx)
-    for (int by = 1; by <= std::min(kp.nc[1], 8); ++by)
-      for (int bz = 1; bz <= std::min(kp.nc[2], 12); ++bz) {
-        const int b[3] = {bx, by, bz};
-        int icells = 1, rcells = 1, nblk = 1;
-        for (int d = 0; d < 3; ++d) {
-          icells *= b[d];
-          rcells *= region_width(kp, d, b[d]);
-          nblk *= (kp.nc[d] + b[d] - 1) / b[d];
-        }
-        if (icells > kMaxBlockCells || rcells > kMaxRegionCells) continue;
-        const double reg = a * rcells * 1.3 + 64.0;
-        if (reg * 16.0 + 24.0 * rcells > 100.0 * 1024.0 && !(bx == 1 && by == 1 && bz == 1)) continue;
-        const double ctas = (double)kp.R * nblk;
-        double score = (a * icells) / (a * rcells);
-        if (ctas < 2.0 * 148) score *= ctas / (2.0 * 148);
-        if (a * icells > 640) score *= 640.0 / (a * icells);
-        if (score > best) { best = score; bb[0] = bx; bb[1] = by; bb[2] = bz; }
-      }
-  kp.nblk = 1;
-  kp.rcells = 1;
-  int icells = 1;
-  for (int d = 0; d < 3; ++d) {
-    kp.b[d] = bb[d];
-    kp.nb[d] = (kp.nc[d] + bb[d] - 1) / bb[d];
-    kp.nblk *= kp.nb[d];
-    kp.rcells *= region_width(kp, d, bb[d]);
-    icells *= bb[d];
-  }
-  set_region_capacity(kp, (int)std::ceil(a * kp.rcells * 1.5 + 64.0));
-  const int want = (int)std::ceil(a * icells * 1.1);
-  kp.bthreads = std::min(512, std::max(64, (want + 31) / 32 * 32));
-}
-
 cph_status run_pfc(Ctx &c, int r) {
   const KParams &kp = c.kp;
   const double pH = c.h_pH[r];
@@ -247,13 +192,6 @@ cph_status check_flags(Ctx &c) {
     c.err = "lambda diverged (|lambda| > 10 or non-finite dV/dlambda)";
     return CPH_E_DIVERGED;
   }
-  if (f[FLAG_REGION_OVERFLOW]) {
-    char buf[160];
-    snprintf(buf, sizeof buf, "neighbour region overflow: %d atoms > capacity %d; results since the last rebuild are invalid",
-             f[FLAG_REGION_MAX], c.kp.rcap);
-    c.err = buf;
-    return CPH_E_STATE;
-  }
   if (f[FLAG_LIST_OVERFLOW]) {
     char buf[160];
     snprintf(buf, sizeof buf, "pair list overflow: %d neighbours > capacity %d; results since the last rebuild are invalid",
@@ -331,7 +269,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   auto bad = [&](const char *m) { c.err = m; return fail_create(ctx, CPH_E_INVALID); };
   if (prm->abi_version != CPH_ABI_VERSION) return bad("abi_version mismatch");
   const int N = sys->n_atoms, R = prm->n_replicas, G = sys->n_groups, T = sys->n_types;
-  if (N < 1 || N > kMaxAtoms) return bad("n_atoms must be in [1, 2^24]");
+  if (N < 1 || N > kMaxAtoms) return bad("n_atoms must be in [1, 2^21]");
   if (R < 1) return bad("n_replicas must be >= 1");
   if (!sys->pos || !sys->mass || !sys->charge || !sys->type || !sys->c6 || !sys->c12)
     return bad("system arrays pos/mass/charge/type/c6/c12 are required");
@@ -460,7 +398,6 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     kp.cap = (int)std::ceil(1.6 * expect + 64.0);
     kp.cap = (kp.cap + 7) / 8 * 8;
   }
-  choose_blocks(kp, N);
   for (int d = 0; d < 3; ++d) kp.K[d] = prm->pme_grid[d];
   kp.K3 = kp.K[0] * kp.K[1] * kp.K[2];
   kp.Kzc = kp.K[2] / 2 + 1;
@@ -627,30 +564,6 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   }
   c.host_step = 0;
   cph_status st = evaluate_here(c);
-  // size the shared-memory region capacity from the regions the first build saw (solute
-  // regions are denser than bulk solvent); re-evaluate once if the estimate was too small
-  if (st == CPH_OK) {
-    int f[FLAG_COUNT];
-    if (cudaStreamSynchronize(c.stream) != cudaSuccess ||
-        cudaMemcpy(f, c.d.flags, sizeof(f), cudaMemcpyDeviceToHost) != cudaSuccess) {
-      c.err = "flag read failed";
-      st = CPH_E_CUDA;
-    } else {
-      const int need = (int)std::ceil(f[FLAG_REGION_MAX] * 1.25) + 64;
-      const bool overflow = f[FLAG_REGION_OVERFLOW] != 0;
-      if (need >= kMaxRegionAtoms || nonbonded_smem_bytes_for(c.kp, need) > 227 * 1024) {
-        c.err = "neighbour region too large for shared memory (dense system?)";
-        st = CPH_E_UNSUPPORTED;
-      } else {
-        set_region_capacity(c.kp, need);
-        if (overflow) {
-          f[FLAG_REGION_OVERFLOW] = 0;
-          cudaMemcpy(c.d.flags, f, sizeof(f), cudaMemcpyHostToDevice);
-          st = evaluate_here(c);
-        }
-      }
-    }
-  }
   if (st == CPH_OK) st = check_flags(c);
   if (st != CPH_OK) {
     cph_status s2 = st;
@@ -875,48 +788,12 @@ cph_status cph_get_pairlist(cph_ctx *ctx, int32_t r, int32_t *pairs, int64_t cap
   CK(cudaMemcpy(nnb.data(), c.d.nnb + base, sizeof(int) * N, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(meta.data(), c.d.meta + base, sizeof(int2) * N, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(nbl.data(), c.d.nbl + (size_t)r * kp.cap * kp.Nst, sizeof(uint32_t) * nbl.size(), cudaMemcpyDeviceToHost));
-  // entries hold region-local indices: rebuild each block's region layout (region.cuh) on
-  // the host from the cell ranges to map them back to sorted slots
-  std::vector<int> cs(kp.ncell + 1);
-  CK(cudaMemcpy(cs.data(), c.d.cell_start + (size_t)r * (kp.ncell + 1), sizeof(int) * cs.size(), cudaMemcpyDeviceToHost));
-  std::vector<std::vector<int>> local2slot(kp.nblk);
-  auto blk_of_cell = [&](int cell) {
-    const int cz = cell % kp.nc[2], cy = (cell / kp.nc[2]) % kp.nc[1], cx = cell / (kp.nc[2] * kp.nc[1]);
-    return ((cx / kp.b[0]) * kp.nb[1] + cy / kp.b[1]) * kp.nb[2] + cz / kp.b[2];
-  };
-  auto layout = [&](int blk) -> const std::vector<int> & {
-    std::vector<int> &v = local2slot[blk];
-    if (!v.empty()) return v;
-    int t = blk;
-    const int Z = t % kp.nb[2]; t /= kp.nb[2];
-    const int Y = t % kp.nb[1], X = t / kp.nb[1];
-    const int B[3] = {X, Y, Z};
-    int o[3], w[3];
-    for (int d = 0; d < 3; ++d) {
-      const int b0 = B[d] * kp.b[d], bw = std::min(kp.b[d], kp.nc[d] - b0);
-      if (kp.ns[d] < 5 || bw + 4 >= kp.nc[d]) { o[d] = 0; w[d] = kp.nc[d]; }
-      else { o[d] = b0 - 2; w[d] = bw + 4; }
-    }
-    for (int a = 0; a < w[0]; ++a)
-      for (int b = 0; b < w[1]; ++b)
-        for (int cc = 0; cc < w[2]; ++cc) {
-          const int gx = (o[0] + a + kp.nc[0]) % kp.nc[0], gy = (o[1] + b + kp.nc[1]) % kp.nc[1];
-          const int gz = (o[2] + cc + kp.nc[2]) % kp.nc[2];
-          const int cell = (gx * kp.nc[1] + gy) * kp.nc[2] + gz;
-          for (int sl = cs[cell]; sl < cs[cell + 1]; ++sl) v.push_back(sl);
-        }
-    return v;
-  };
   std::vector<std::pair<int, int>> out;
-  int cell = 0;
   for (size_t i = 0; i < N; ++i) {
-    while (cs[cell + 1] <= (int)i) ++cell;
-    const std::vector<int> &l2s = layout(blk_of_cell(cell));
     const int oi = meta[i].x;
     for (int k = 0; k < std::min(nnb[i], kp.cap); ++k) {
-      const int jl = (int)(nbl[(size_t)k * kp.Nst + i] & kEntryJMask);
-      if (jl >= (int)l2s.size()) { c.err = "pair list entry outside its region"; return CPH_E_STATE; }
-      const int oj = meta[l2s[jl]].x;
+      const int j = (int)(nbl[(size_t)k * kp.Nst + i] & kEntryJMask);
+      const int oj = meta[j].x;
       if (oi < oj) out.emplace_back(oi, oj);
     }
   }

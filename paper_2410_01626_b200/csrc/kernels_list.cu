@@ -2,14 +2,13 @@
 //
 // Every nstlist steps: atoms are binned into cells of edge >= rlist/2 (stencil +-2, or the
 // whole dimension when it has fewer than 5 cells), counting-sorted by cell, ordered by
-// (z, original index) inside each cell (deterministic layout), positions are wrapped into the
-// box, and all per-atom arrays are permuted.  Then each atom gets a FULL neighbour list (both directions, so the pair kernel
+// original index inside each cell (deterministic layout), and all per-atom arrays are
+// permuted.  Then each atom gets a FULL neighbour list (both directions, so the pair kernel
 // needs no atomics) of the non-excluded atoms with float32 d^2 < rlist^2, evaluated with the
 // canonical round-to-nearest, no-contraction formula of DESIGN.md R14 so that the list is
-// bit-exact against the oracle's.  Entries: region-local index (16 bits) | LJ type (5 bits) |
-// periodic image code (5 bits); stored k-major (nbl[k][i]) so a warp reads 128 contiguous
-// bytes per neighbour index.
-#include "region.cuh"
+// bit-exact against the oracle's.  Entries: sorted slot (24 bits) | LJ type (8 bits); stored
+// k-major (nbl[k][i]) so a warp reads 128 contiguous bytes per neighbour index.
+#include "cph_device.cuh"
 
 namespace cph {
 
@@ -147,88 +146,148 @@ __global__ void k_copy_back(KParams kp, DevBufs d) {
   d.meta[idx] = d.meta_alt[idx];
 }
 
-// One CTA per block: stage the block's region in shared memory, then every thread takes
-// i atoms of the block and tests the atoms of its +-2 cell stencil (all in shared memory)
-// with the canonical formula.  Entries hold region-local indices (region.cuh).
-__global__ void __launch_bounds__(512) k_build_list(KParams kp, DevBufs d) {
-  extern __shared__ float4 s_x[];                       // [rcap]
-  __shared__ int s_coff[kMaxRegionCells + 1], s_cglob[kMaxRegionCells];
-  __shared__ int s_ioff[kMaxBlockCells + 1], s_iglob[kMaxBlockCells];
-  const int r = blockIdx.y;
+// One warp per cell: the i atoms are the cell's atoms (one per lane, chunks of 32), and every
+// stencil cell's atoms are staged through shared memory (coalesced loads, broadcast reads),
+// so the loop structure is uniform across the warp.
+__global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
+  const int r = blockIdx.y, c = blockIdx.x;
+  const int lane = threadIdx.x;
   const size_t base = (size_t)r * kp.Nst;
   const float4 *xq = d.xyzq + base;
   const int2 *meta = d.meta + base;
   const int *start = d.cell_start + (size_t)r * (kp.ncell + 1);
-  const Region g = block_region(kp, blockIdx.x);
-  region_tables(kp, g, start, s_coff, s_cglob, s_ioff, s_iglob);
-  const int nreg = s_coff[g.ncells];
-  if (threadIdx.x == 0) {
-    atomicMax(&d.flags[FLAG_REGION_MAX], nreg);
-    if (nreg > kp.rcap) d.flags[FLAG_REGION_OVERFLOW] = 1;
-  }
-  region_stage(xq, start, g, s_coff, s_cglob, s_x, kp.rcap);
-  __syncthreads();
+  __shared__ float4 sx[32];
+  __shared__ int sj[32];
+  __shared__ float4 sbc[8], sbh[8];    // cluster box centres and half extents
+  const int cz = c % kp.nc[2], cy = (c / kp.nc[2]) % kp.nc[1], cx = c / (kp.nc[2] * kp.nc[1]);
+  const int ib = start[c], ie = start[c + 1];
   const float3 Lbox = make_float3(kp.L[0], kp.L[1], kp.L[2]);
   const float3 Linv = make_float3(kp.invL[0], kp.invL[1], kp.invL[2]);
   const float rlist2 = kp.rlist2;
-  const int nI = s_ioff[g.nbcells];
-  for (int t = threadIdx.x; t < nI; t += blockDim.x) {
-    int bc;
-    const int i = block_atom_slot(s_ioff, s_iglob, start, g.nbcells, t, &bc);
-    const float4 xi = xq[i];
-    const int orig = meta[i].x;
-    const int eb = d.excl_ptr[orig], ee = d.excl_ptr[orig + 1];
-    const int cz = g.b0[2] + bc % g.bw[2];
-    const int cy = g.b0[1] + (bc / g.bw[2]) % g.bw[1];
-    const int cx = g.b0[0] + bc / (g.bw[2] * g.bw[1]);
-    uint32_t *out = d.nbl + (size_t)r * kp.cap * kp.Nst + i;
+  const float rlist2_pre = kp.rlist2 * 1.001f;
+  // stencil tables (cell index and, for +-2 stencils, the uniform periodic image shift
+  // L * floor(raw / nc) of that j-cell; dimensions with < 5 cells use per-lane images)
+  __shared__ int s_cell[3][8];
+  __shared__ float s_wsh[3][8];
+  if (lane < 24) {
+    const int dd = lane >> 3, o = lane & 7;
+    const int cdim = dd == 0 ? cx : (dd == 1 ? cy : cz);
+    if (o < kp.ns[dd]) {
+      const int raw = cdim + kp.so[dd] + o;
+      s_cell[dd][o] = (raw + 2 * kp.nc[dd]) % kp.nc[dd];
+      s_wsh[dd][o] = kp.ns[dd] == 5 ? kp.L[dd] * (float)((raw + kp.nc[dd]) / kp.nc[dd] - 1) : 0.f;
+    }
+  }
+  __syncwarp();
+  for (int i0 = ib; i0 < ie; i0 += 32) {
+    const int i = i0 + lane;
+    const bool valid = i < ie;
+    const float4 xi = valid ? xq[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int orig = valid ? meta[i].x : 0;
+    const int eb = valid ? d.excl_ptr[orig] : 0, ee = valid ? d.excl_ptr[orig + 1] : 0;
+    uint32_t *out = d.nbl + (size_t)r * kp.cap * kp.Nst + (valid ? i : 0);
     const size_t ostride = kp.Nst;
     int cnt = 0;
     for (int ox = 0; ox < kp.ns[0]; ++ox) {
-      const int gx = (cx + kp.so[0] + ox + 2 * kp.nc[0]) % kp.nc[0];
+      const int gx = s_cell[0][ox];
+      const float wsx = s_wsh[0][ox];
       for (int oy = 0; oy < kp.ns[1]; ++oy) {
-        const int gy = (cy + kp.so[1] + oy + 2 * kp.nc[1]) % kp.nc[1];
+        const int gy = s_cell[1][oy];
+        const float wsy = s_wsh[1][oy];
         for (int oz = 0; oz < kp.ns[2]; ++oz) {
-          const int gz = (cz + kp.so[2] + oz + 2 * kp.nc[2]) % kp.nc[2];
-          const int lc = region_local(kp, g, gx, gy, gz);
-          const int jb = s_coff[lc], je = min(s_coff[lc + 1], kp.rcap);
-          const int gstart = start[s_cglob[lc]] - jb;       // global slot = local + gstart
-          for (int jl = jb; jl < je; ++jl) {
-            const float4 xj = s_x[jl];
-            // canonical formula (R14): dx = x_j - x_i ; dx -= L rint(dx / L);
-            // positions are wrapped into [0, L] at the rebuild, so |dx / L| <= 1 and
-            // rint(t) == (t > 0.5) - (t < -0.5) exactly (ties to even)
-            const float rx = __fsub_rn(xj.x, xi.x), ry = __fsub_rn(xj.y, xi.y), rz = __fsub_rn(xj.z, xi.z);
-            const float kx = rint_unit(__fmul_rn(rx, Linv.x));
-            const float ky = rint_unit(__fmul_rn(ry, Linv.y));
-            const float kz = rint_unit(__fmul_rn(rz, Linv.z));
-            const float dx = __fsub_rn(rx, __fmul_rn(Lbox.x, kx));
-            const float dy = __fsub_rn(ry, __fmul_rn(Lbox.y, ky));
-            const float dz = __fsub_rn(rz, __fmul_rn(Lbox.z, kz));
-            const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-            if (!(d2 < rlist2)) continue;
-            const int j = jl + gstart;
-            if (j == i) continue;
-            const int2 mj = meta[j];
-            if (ee > eb) {
-              bool ex = false;
-              for (int e = eb; e < ee; ++e) ex |= (d.excl_idx[e] == mj.x);
-              if (ex) continue;
+          const int cc = (gx * kp.nc[1] + gy) * kp.nc[2] + s_cell[2][oz];
+          const float wsz = s_wsh[2][oz];
+          const int jb = start[cc], je = start[cc + 1];
+          for (int j0 = jb; j0 < je; j0 += 32) {
+            const int nj = min(32, je - j0);
+            __syncwarp();
+            if (lane < nj) {
+              const int j = j0 + lane;
+              sx[lane] = xq[j];
+              sj[lane] = j | ((meta[j].y & (int)kEntryTypeMask) << kEntryTypeShift);
             }
-            const int code = (int)(kx * 9.0f + ky * 3.0f + kz) + 13;
-            if (cnt < kp.cap)
-              *out = (uint32_t)jl | ((uint32_t)(mj.y & (int)kEntryTypeMask) << kEntryTypeShift) |
-                     ((uint32_t)code << kEntryImgShift);
-            out += ostride;
-            ++cnt;
+            __syncwarp();
+            // bounding box of each cluster of 4 consecutive staged atoms (z-sorted in the cell)
+            {
+              float4 p = sx[min(lane, nj - 1)];
+              float lo_x = p.x, lo_y = p.y, lo_z = p.z, hi_x = p.x, hi_y = p.y, hi_z = p.z;
+#pragma unroll
+              for (int o = 1; o < 4; o <<= 1) {
+                lo_x = fminf(lo_x, __shfl_xor_sync(0xffffffffu, lo_x, o));
+                lo_y = fminf(lo_y, __shfl_xor_sync(0xffffffffu, lo_y, o));
+                lo_z = fminf(lo_z, __shfl_xor_sync(0xffffffffu, lo_z, o));
+                hi_x = fmaxf(hi_x, __shfl_xor_sync(0xffffffffu, hi_x, o));
+                hi_y = fmaxf(hi_y, __shfl_xor_sync(0xffffffffu, hi_y, o));
+                hi_z = fmaxf(hi_z, __shfl_xor_sync(0xffffffffu, hi_z, o));
+              }
+              if ((lane & 3) == 0) {
+                sbc[lane >> 2] = make_float4(0.5f * (lo_x + hi_x) + wsx, 0.5f * (lo_y + hi_y) + wsy,
+                                             0.5f * (lo_z + hi_z) + wsz, 0.f);
+                sbh[lane >> 2] = make_float4(0.5f * (hi_x - lo_x), 0.5f * (hi_y - lo_y), 0.5f * (hi_z - lo_z), 0.f);
+              }
+              __syncwarp();
+            }
+            if (!valid) continue;
+            // four candidates (one cluster) per pass (ILP); appends stay in candidate order
+            for (int t0 = 0; t0 < nj; t0 += 4) {
+              // conservative prefilter: distance from x_i to the cluster box (nearest image);
+              // the box contains its atoms, so a rejected cluster cannot hold a list pair
+              // (margin 1e-3 relative on d^2 covers the float rounding of this estimate)
+              {
+                const float4 bc = sbc[t0 >> 2], bh = sbh[t0 >> 2];
+                float cx_ = bc.x - xi.x, cy_ = bc.y - xi.y, cz_ = bc.z - xi.z;
+                if (kp.ns[0] != 5) cx_ -= Lbox.x * rintf(cx_ * Linv.x);
+                if (kp.ns[1] != 5) cy_ -= Lbox.y * rintf(cy_ * Linv.y);
+                if (kp.ns[2] != 5) cz_ -= Lbox.z * rintf(cz_ * Linv.z);
+                const float gx_ = fmaxf(fabsf(cx_) - bh.x, 0.f), gy_ = fmaxf(fabsf(cy_) - bh.y, 0.f),
+                            gz_ = fmaxf(fabsf(cz_) - bh.z, 0.f);
+                if (gx_ * gx_ + gy_ * gy_ + gz_ * gz_ > rlist2_pre) continue;
+              }
+              float d2v[4], kxv[4], kyv[4], kzv[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float4 xj = sx[min(t0 + u, nj - 1)];
+                // canonical formula (R14): dx = x_j - x_i ; dx -= L rint(dx / L)
+                const float rx = __fsub_rn(xj.x, xi.x), ry = __fsub_rn(xj.y, xi.y), rz = __fsub_rn(xj.z, xi.z);
+                // positions are wrapped into [0, L] at the rebuild, so |dx / L| <= 1 and
+                // rint(t) == (t > 0.5) - (t < -0.5) exactly (ties to even); the selects run on
+                // the ALU pipe instead of the XU pipe FRND needs
+                kxv[u] = rint_unit(__fmul_rn(rx, Linv.x));
+                kyv[u] = rint_unit(__fmul_rn(ry, Linv.y));
+                kzv[u] = rint_unit(__fmul_rn(rz, Linv.z));
+                const float dx = __fsub_rn(rx, __fmul_rn(Lbox.x, kxv[u]));
+                const float dy = __fsub_rn(ry, __fmul_rn(Lbox.y, kyv[u]));
+                const float dz = __fsub_rn(rz, __fmul_rn(Lbox.z, kzv[u]));
+                d2v[u] = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                if (t0 + u >= nj || !(d2v[u] < rlist2)) continue;
+                const int code = (int)(kxv[u] * 9.0f + kyv[u] * 3.0f + kzv[u]) + 13;
+                const int je_ = sj[t0 + u] | (code << kEntryImgShift);
+                const int j = je_ & (int)kEntryJMask;
+                if (j == i) continue;
+                if (ee > eb) {
+                  const int oj = meta[j].x;
+                  bool ex = false;
+                  for (int e = eb; e < ee; ++e) ex |= (d.excl_idx[e] == oj);
+                  if (ex) continue;
+                }
+                if (cnt < kp.cap) *out = (uint32_t)je_;
+                out += ostride;
+                ++cnt;
+              }
+            }
           }
         }
       }
     }
-    d.nnb[base + i] = cnt;
-    if (cnt > kp.cap) {
-      d.flags[FLAG_LIST_OVERFLOW] = 1;
-      atomicMax(&d.flags[FLAG_MAX_NNB], cnt);
+    if (valid) {
+      d.nnb[base + i] = cnt;
+      if (cnt > kp.cap) {
+        d.flags[FLAG_LIST_OVERFLOW] = 1;
+        atomicMax(&d.flags[FLAG_MAX_NNB], cnt);
+      }
     }
   }
 }
@@ -243,13 +302,7 @@ int launch_rebuild(Ctx &c, cudaStream_t s) {
   k_cell_sort<<<dim3((kp.ncell + 127) / 128, kp.R), 128, 0, s>>>(kp, c.d);
   k_permute<<<ga, 128, 0, s>>>(kp, c.d);
   k_copy_back<<<ga, 128, 0, s>>>(kp, c.d);
-  const size_t smem = sizeof(float4) * (size_t)kp.rcap;
-  static size_t configured = 48 * 1024;
-  if (smem > configured) {
-    cudaFuncSetAttribute(k_build_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
-  }
-  k_build_list<<<dim3(kp.nblk, kp.R), kp.bthreads, smem, s>>>(kp, c.d);
+  k_build_list<<<dim3(kp.ncell, kp.R), 32, 0, s>>>(kp, c.d);
   return 7;
 }
 

@@ -1,10 +1,8 @@
 // Real-space Ewald + Lennard-Jones pair kernel that also accumulates phi_i.
 //
-// One CTA per block of cells (region.cuh): the block's region (every cell within +-2 cells)
-// is staged in shared memory, then each thread takes one i atom of the block and walks its
-// full neighbour list, reading neighbours from shared memory (list entries are region-local
-// indices).  Forces and potentials are accumulated in registers with no atomics and in a
-// fixed order (run-to-run deterministic).  For r < rc:
+// One thread per (sorted) atom i walks its full neighbour list, so forces and potentials are
+// accumulated in registers with no atomics and in a fixed order (run-to-run deterministic).
+// For r < rc:
 //   E_ij  = c12/r^12 - c6/r^6 + f q_i q_j erfc(beta r)/r
 //   phi_i += q_j erfc(beta r)/r
 //   F_i   += [f q_i q_j (erfc(beta r)/r + 2 beta/sqrt(pi) e^{-beta^2 r^2}) + 12 c12/r^12 - 6 c6/r^6] / r^2 * (x_i - x_j)
@@ -14,16 +12,16 @@
 // Warps that contain a lambda atom also accumulate phi in fp64 (dV/dlambda at 2e-5; BASELINE
 // "fp64 lambda reductions"); on energy steps the per-atom sums are fp64 as well.
 // Compiled with -ftz=true: no denormal fix-ups around MUFU.RSQ / RCP / EX2.
-#include "region.cuh"
+#include "cph_device.cuh"
 
 namespace cph {
 
 template <bool ENERGY, bool PHI64>
-__device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, const float4 *__restrict__ xs,
-                                        const float4 *__restrict__ xg, const float2 *__restrict__ ljf,
-                                        const float2 *__restrict__ lje, const float4 *__restrict__ shift, int r,
-                                        int i, bool valid, uint32_t self_local, float4 xi, int ti, int lslot, int n,
-                                        int nmax, double *e_lj, double *e_real, double *e_excl) {
+__device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, const float4 *__restrict__ xq,
+                                        const float2 *__restrict__ ljf, const float2 *__restrict__ lje,
+                                        const float4 *__restrict__ shift, int r, int i, bool valid,
+                                        float4 xi, int ti, int lslot, int n, int nmax,
+                                        double *e_lj, double *e_real, double *e_excl) {
   const float qif = kp.fcoul * xi.w;
   float fx = 0.f, fy = 0.f, fz = 0.f, phi = 0.f;
   double phid = 0.0, elj = 0.0;        // fp64 only in lambda warps / on energy steps
@@ -37,7 +35,8 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
   // Entries past a lane's own count point at the lane's own atom with zero shift (r2 = 0,
   // masked), so a chunk's U loads are unconditional and the next chunk's entries are
   // prefetched while the current chunk computes.
-  const uint32_t self = self_local | ((uint32_t)ti << kEntryTypeShift) | (13u << kEntryImgShift);
+  const uint32_t self = (uint32_t)(valid ? i : 0) | ((uint32_t)ti << kEntryTypeShift) |
+                        (13u << kEntryImgShift);
   uint32_t en[U];
   const int stride = kp.Nst;
 #pragma unroll
@@ -49,7 +48,7 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       e[u] = en[u];
-      xj[u] = xs[e[u] & kEntryJMask];
+      xj[u] = __ldg(&xq[(int)(e[u] & kEntryJMask)]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) en[u] = k0 + U + u < n ? __ldcs(Lk + u * stride) : self;
@@ -92,7 +91,7 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
     const int eb = d.excl_ptr[orig], ee = d.excl_ptr[orig + 1];
     for (int e = eb; e < ee; ++e) {
       const int js = d.iperm[(size_t)r * kp.N + d.excl_idx[e]];
-      const float4 xj = xg[js];
+      const float4 xj = xq[js];
       float dx = xi.x - xj.x, dy = xi.y - xj.y, dz = xi.z - xj.z;
       dx -= Lx * rintf(dx * iLx);
       dy -= Ly * rintf(dy * iLy);
@@ -116,27 +115,16 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
     if (PHI64 && lslot >= 0) d.phi64_nb[(size_t)r * kp.nlam + lslot] = phid + phxd;
   }
   if (ENERGY && valid) {
-    *e_lj += 0.5 * elj;
-    *e_real += 0.5 * (double)kp.fcoul * (double)xi.w * phid;
-    *e_excl += 0.5 * (double)kp.fcoul * (double)xi.w * phxd;
+    *e_lj = 0.5 * elj;
+    *e_real = 0.5 * (double)kp.fcoul * (double)xi.w * phid;
+    *e_excl = 0.5 * (double)kp.fcoul * (double)xi.w * phxd;
   }
 }
 
-// dynamic shared memory layout of the pair kernel
-__host__ __device__ inline size_t nb_smem_bytes(const KParams &kp) {
-  return sizeof(float4) * (size_t)kp.rcap + 2 * sizeof(float2) * kp.T * kp.T + sizeof(float4) * 27 +
-         sizeof(int) * (2 * (size_t)kp.rcells + 1 + 2 * kMaxBlockCells + 1);
-}
-
-__global__ void __launch_bounds__(512) k_nonbonded(KParams kp, DevBufs d, int step_offset) {
-  extern __shared__ float4 s_x[];                                   // [rcap]
-  float2 *s_ljf = reinterpret_cast<float2 *>(s_x + kp.rcap);        // (6 c6, 12 c12)
-  float2 *s_lje = s_ljf + kp.T * kp.T;                              // (c6, c12)
-  float4 *s_shift = reinterpret_cast<float4 *>(s_lje + kp.T * kp.T);  // L * (kx, ky, kz)
-  int *s_coff = reinterpret_cast<int *>(s_shift + 27);
-  int *s_cglob = s_coff + kp.rcells + 1;
-  int *s_ioff = s_cglob + kp.rcells;
-  int *s_iglob = s_ioff + kMaxBlockCells + 1;
+__global__ void __launch_bounds__(128) k_nonbonded(KParams kp, DevBufs d, int step_offset) {
+  __shared__ float2 s_ljf[kMaxTypes * kMaxTypes];   // (6 c6, 12 c12) for forces
+  __shared__ float2 s_lje[kMaxTypes * kMaxTypes];   // (c6, c12) for energies
+  __shared__ float4 s_shift[27];                    // image shift L * (kx, ky, kz)
   for (int t = threadIdx.x; t < kp.T * kp.T; t += blockDim.x) {
     const float2 c = d.ljtab[t];
     s_ljf[t] = c;
@@ -147,45 +135,28 @@ __global__ void __launch_bounds__(512) k_nonbonded(KParams kp, DevBufs d, int st
     s_shift[code] = make_float4(kp.L[0] * (float)(code / 9 - 1), kp.L[1] * (float)((code / 3) % 3 - 1),
                                 kp.L[2] * (float)(code % 3 - 1), 0.f);
   }
-  const int r = blockIdx.y;
-  const float4 *xg = d.xyzq + (size_t)r * kp.Nst;
-  const int *start = d.cell_start + (size_t)r * (kp.ncell + 1);
-  const Region g = block_region(kp, blockIdx.x);
-  region_tables(kp, g, start, s_coff, s_cglob, s_ioff, s_iglob);
-  region_stage(xg, start, g, s_coff, s_cglob, s_x, kp.rcap);
   __syncthreads();
+  const int r = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < kp.N;
   const long long m = *d.step + step_offset;
   const bool energy = is_energy_step(m, *d.end_step, kp.nstenergy);
-  const int nI = s_ioff[g.nbcells];
-  const int lane = threadIdx.x & 31;
+  const size_t idx = (size_t)r * kp.Nst + (valid ? i : 0);
+  const float4 xi = d.xyzq[idx];
+  const int2 mi = d.meta[idx];
+  const int ti = mi.y & 0xFF;
+  const int lslot = valid ? (mi.y >> 8) - 1 : -1;
+  const int n = valid ? d.nnb[idx] : 0;
+  const int nmax = __reduce_max_sync(0xffffffffu, n);
+  const bool warp_lam = __any_sync(0xffffffffu, lslot >= 0);
+  const float4 *xq = d.xyzq + (size_t)r * kp.Nst;
   double elj = 0.0, ere = 0.0, eex = 0.0;
-  for (int t0 = threadIdx.x - lane; t0 < nI; t0 += blockDim.x) {
-    const int t = t0 + lane;
-    const bool valid = t < nI;
-    int bc = 0, i = 0;
-    uint32_t self_local = 0;
-    if (valid) {
-      i = block_atom_slot(s_ioff, s_iglob, start, g.nbcells, t, &bc);
-      const int cz = g.b0[2] + bc % g.bw[2];
-      const int cy = g.b0[1] + (bc / g.bw[2]) % g.bw[1];
-      const int cx = g.b0[0] + bc / (g.bw[2] * g.bw[1]);
-      self_local = (uint32_t)(s_coff[region_local(kp, g, cx, cy, cz)] + (t - s_ioff[bc]));
-    }
-    const size_t idx = (size_t)r * kp.Nst + i;
-    const float4 xi = xg[i];
-    const int2 mi = d.meta[idx];
-    const int ti = mi.y & 0xFF;
-    const int lslot = valid ? (mi.y >> 8) - 1 : -1;
-    const int n = valid ? d.nnb[idx] : 0;
-    const int nmax = __reduce_max_sync(0xffffffffu, n);
-    const bool warp_lam = __any_sync(0xffffffffu, lslot >= 0);
-    if (warp_lam) {
-      if (energy) nb_atom<true, true>(kp, d, s_x, xg, s_ljf, s_lje, s_shift, r, i, valid, self_local, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
-      else nb_atom<false, true>(kp, d, s_x, xg, s_ljf, s_lje, s_shift, r, i, valid, self_local, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
-    } else {
-      if (energy) nb_atom<true, false>(kp, d, s_x, xg, s_ljf, s_lje, s_shift, r, i, valid, self_local, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
-      else nb_atom<false, false>(kp, d, s_x, xg, s_ljf, s_lje, s_shift, r, i, valid, self_local, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
-    }
+  if (warp_lam) {
+    if (energy) nb_atom<true, true>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
+    else nb_atom<false, true>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
+  } else {
+    if (energy) nb_atom<true, false>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
+    else nb_atom<false, false>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
   }
   if (energy) {
     double *e = d.erec + ((size_t)(m & 1) * kp.R + r) * kNE;
@@ -195,17 +166,9 @@ __global__ void __launch_bounds__(512) k_nonbonded(KParams kp, DevBufs d, int st
   }
 }
 
-size_t nonbonded_smem(const KParams &kp) { return nb_smem_bytes(kp); }
-
 int launch_nonbonded(Ctx &c, cudaStream_t s, int step_offset) {
-  const size_t smem = nb_smem_bytes(c.kp);
-  static size_t configured = 48 * 1024;
-  if (smem > configured) {
-    cudaFuncSetAttribute(k_nonbonded, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
-  }
-  dim3 grid(c.kp.nblk, c.kp.R);
-  k_nonbonded<<<grid, c.kp.bthreads, smem, s>>>(c.kp, c.d, step_offset);
+  dim3 grid((c.kp.N + 127) / 128, c.kp.R);
+  k_nonbonded<<<grid, 128, 0, s>>>(c.kp, c.d, step_offset);
   return 1;
 }
 
