@@ -182,3 +182,98 @@ def test_fixed_lambda_ti_mode(cph):
     mean, n = ctx.cph_get_ti_means(0)
     assert n == 6
     np.testing.assert_allclose(mean, acc / 6, rtol=1e-12, atol=1e-12)
+
+
+def test_gpu_sampling_follows_hh_when_coulomb_dvdl_vanishes(cph):
+    """States with equal charges make the Coulomb dV/dlambda exactly zero, so lambda samples
+    only the bias: with PFC the deprotonated fraction is 1/(10^(pKa-pH)+1) (PAPER.md:979,
+    Eq. 4) and His tautomers split delta:eps = 10^(pKa_eps - pKa_delta) (Table 2)."""
+    import copy
+    s = copy.deepcopy(small_system())
+    s.state_q[:, 2] = s.state_q[:, 0]
+    s.state_q[:, 3] = s.state_q[:, 0]
+    s.vmm[:] = 0.0
+    levels = np.array([3.4, 4.4, 5.4, 6.5])
+    per = 128                          # replicas per pH: ~3 sigma margin at 0.03
+    pH = np.repeat(levels, per)
+    R = len(pH)
+    # start from the target populations (end states), so the run samples the stationary law
+    rng = np.random.default_rng(5)
+    p_glu = 1.0 / (10 ** (4.4 - pH) + 1.0)
+    w = np.stack([np.ones(R), 10 ** (pH - 6.53), 10 ** (pH - 6.92)], 1)
+    his_state = np.array([rng.choice(3, p=wi / wi.sum()) for wi in w])
+    lam0 = np.stack([(rng.random(R) < p_glu).astype(float), (his_state > 0).astype(float),
+                     (his_state == 2).astype(float)], 1)
+    ctx = cph.cph_create(s, pH, replica_seeds(7, R), lambda0=lam0, barrier=2.0, nstout=20,
+                         frame_capacity=2048, vel_replicas=np.stack([make_velocities(s, r) for r in range(R)]))
+    ctx.cph_step(5000)                 # equilibrate 10 ps
+    for r in range(R):
+        ctx.cph_get_frames(r)          # drop equilibration frames
+    ctx.cph_step(30000)                # 60 ps
+    glu = np.zeros(len(levels))
+    his_d = np.zeros(len(levels))
+    his_e = np.zeros(len(levels))
+    for k in range(len(levels)):
+        lp, dl, el = [], [], []
+        for r in range(k * per, (k + 1) * per):
+            fr, dropped = ctx.cph_get_frames(r)
+            assert dropped == 0
+            lp.append(fr[:, 0])
+            deprot = fr[:, 1] >= 0.5
+            dl.append(np.mean(deprot & (fr[:, 2] < 0.5)))
+            el.append(np.mean(deprot & (fr[:, 2] >= 0.5)))
+        glu[k] = np.mean(np.concatenate(lp) >= 0.5)
+        his_d[k], his_e[k] = np.mean(dl), np.mean(el)
+    hh = 1.0 / (10 ** (4.4 - levels) + 1.0)
+    print("glu", glu, hh)
+    assert np.all(np.abs(glu - hh) < 0.03)
+    pk_d, pk_e = 6.53, 6.92
+    prot = 1.0 / (1 + 10 ** (levels - pk_d) + 10 ** (levels - pk_e))
+    print("his delta", his_d, prot * 10 ** (levels - pk_d), "eps", his_e, prot * 10 ** (levels - pk_e))
+    assert np.all(np.abs(his_d - prot * 10 ** (levels - pk_d)) < 0.03)
+    assert np.all(np.abs(his_e - prot * 10 ** (levels - pk_e)) < 0.03)
+
+
+def test_full_size_c5_sampled_parity(cph):
+    """BASELINE's largest config (250k atoms, K=128) in the bench launch configuration: sampled
+    atoms' phi and forces and every group's dV/dlambda against the oracle computed one by one."""
+    from oracle import ewald as OE
+    from oracle import pme as OP
+    from oracle.charges import charges
+    from oracle.units import F_COUL
+    s = make_system(5)
+    lam0 = np.random.default_rng(2).uniform(0, 1, (1, s.n_coords))
+    ctx = cph.cph_create(s, [5.0], [11], lambda0=lam0)
+    f, phi = ctx.cph_get_forces(0)
+    coul, _ = ctx.cph_get_dvdl(0)
+    q, dq = charges(s, lam0[0])
+    beta = OE.ewald_beta(1.0, 1e-5)
+    x = s.pos.astype(np.float64)
+    rec = OP.pme(x, q, s.box, beta, s.pme_grid, 4)
+    idx = np.concatenate([s.group_atoms, np.random.default_rng(0).choice(s.n_atoms, 64, replace=False)])
+    idx = np.unique(idx)
+    phr, Fr = OE.real_space_at(idx, x, q, s.type, s.c6, s.c12, s.box, 1.0, beta, s.excl)
+    ex = OE.exclusion_correction(x, q, s.box, beta, s.excl)
+    _, phis = OE.self_term(q, beta)
+    _, phin = OE.net_charge_term(q, s.box, beta)
+    phi_ref = phr + ex["phi"][idx] + rec["phi"][idx] + phis[idx] + phin[idx]
+    F_ref = Fr + ex["F"][idx] + rec["F"][idx]
+    assert np.linalg.norm(phi[idx] - phi_ref) / np.linalg.norm(phi_ref) < 2e-5
+    assert np.linalg.norm(f[idx] - F_ref) / np.linalg.norm(F_ref) < 2e-5
+    # dV/dlambda per coordinate from the sampled phi of every lambda atom
+    pos = {a: k for k, a in enumerate(idx)}
+    from oracle.charges import coord_ptr
+    cp = coord_ptr(s.group_kind)
+    ref = np.zeros(s.n_coords)
+    mag = np.zeros(s.n_coords)
+    for g in range(s.n_groups):
+        for k in range(s.group_ptr[g], s.group_ptr[g + 1]):
+            p = phi_ref[pos[s.group_atoms[k]]]
+            ref[cp[g]] += F_COUL * dq[k, 0] * p
+            mag[cp[g]] += abs(F_COUL * dq[k, 0] * p)
+            if s.group_kind[g] == 3:
+                ref[cp[g] + 1] += F_COUL * dq[k, 1] * p
+                mag[cp[g] + 1] += abs(F_COUL * dq[k, 1] * p)
+    err = np.abs(coul - ref) / np.maximum(np.abs(ref), mag)
+    print("C5 dvdl max rel", err.max())
+    assert err.max() < 2e-5
