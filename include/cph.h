@@ -186,8 +186,10 @@ cph_status cph_get_positions(cph_ctx *ctx, int32_t replica, float *pos, float *v
  * indices) with float32 d^2 < rlist^2, lexicographically sorted, as [2*n].
  * If cap < n nothing is written and *n tells the size needed. */
 cph_status cph_get_pairlist(cph_ctx *ctx, int32_t replica, int32_t *pairs, int64_t cap, int64_t *n);
-/* Mean dV/dlambda (coul+bias) per coordinate over the steps since create or the
- * last call (mode 1, TI), and the number of samples. */
+/* Fixed-lambda TI (mode 1): mean of the Coulomb dV/dlambda = f sum (dq/dl) phi per
+ * coordinate over the steps completed since create or the last cph_set_state(_all)
+ * (which restart the accumulators), and the number of samples; this is the
+ * <dH_ref/dlambda> = <dV_coul/dlambda> the Vmm calibration fits. */
 cph_status cph_get_ti_means(cph_ctx *ctx, int32_t replica, double *mean /*[C]*/, int64_t *n_samples);
 /* Checkpoint of one replica: size query with buf == NULL (*n gets bytes). */
 cph_status cph_get_state(cph_ctx *ctx, int32_t replica, void *buf, int64_t cap, int64_t *n);

@@ -880,6 +880,9 @@ cph_status cph_set_state(cph_ctx *ctx, int32_t r, const void *buf, int64_t nbyte
   cph_status st = check_replica(c, r);
   if (st || (st = cph_sync(ctx))) return st;
   if ((st = upload_state(c, r, buf, nbytes))) return st;
+  // a new configuration: TI accumulators restart
+  CK(cudaMemsetAsync(c.d.ti_sum, 0, sizeof(double) * (size_t)c.kp.R * c.kp.C, c.stream));
+  CK(cudaMemsetAsync(c.d.ti_n, 0, sizeof(long long), c.stream));
   if ((st = evaluate_here(c))) return st;
   return check_flags(c);
 }
@@ -907,6 +910,9 @@ cph_status cph_set_state_all(cph_ctx *ctx, const void *buf, int64_t nbytes) {
   if (nbytes < one * c.kp.R) { c.err = "state blob too small"; return CPH_E_INVALID; }
   for (int r = 0; r < c.kp.R; ++r)
     if ((st = upload_state(c, r, (const char *)buf + (size_t)r * one, one))) return st;
+  // a new configuration: TI accumulators restart
+  CK(cudaMemsetAsync(c.d.ti_sum, 0, sizeof(double) * (size_t)c.kp.R * c.kp.C, c.stream));
+  CK(cudaMemsetAsync(c.d.ti_n, 0, sizeof(long long), c.stream));
   if ((st = evaluate_here(c))) return st;
   return check_flags(c);
 }

@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
     }
     kel += 0.5 * kp.m_lam * v * v;
     if (frame) d.frames[((size_t)r * kp.fcap + fslot) * kp.C + c] = (float)l;
-    if (!dyn && mode == 1) d.ti_sum[ix] += dv;
+    if (!dyn && mode == 1) d.ti_sum[ix] += d.dvdl_coul[ix];   // <dV_coul/dlambda>
     if (!(fabs(l) <= 10.0) || !isfinite(dv)) atomicOr(&d.flags[FLAG_DIVERGED], 1);
   }
   kel = block_sum_d(kel);

@@ -96,6 +96,16 @@ __device__ __forceinline__ float rint_unit(float t) {
 // order each cell's atoms by (wrapped z, original index): a deterministic layout in which
 // 4 consecutive atoms of a cell form a compact z-slab "cluster" for the list prefilter
 // (insertion sort; cells hold ~20-60 atoms)
+// the canonical list decision for one pair (R14), used for fast-path candidates
+// inside the rounding band
+__device__ __forceinline__ bool canonical_in(float4 xj, float4 xi, float3 Lbox, float3 Linv, float rlist2) {
+  const float rx = __fsub_rn(xj.x, xi.x), ry = __fsub_rn(xj.y, xi.y), rz = __fsub_rn(xj.z, xi.z);
+  const float dx = __fsub_rn(rx, __fmul_rn(Lbox.x, rint_unit(__fmul_rn(rx, Linv.x))));
+  const float dy = __fsub_rn(ry, __fmul_rn(Lbox.y, rint_unit(__fmul_rn(ry, Linv.y))));
+  const float dz = __fsub_rn(rz, __fmul_rn(Lbox.z, rint_unit(__fmul_rn(rz, Linv.z))));
+  return __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz)) < rlist2;
+}
+
 __global__ void k_cell_sort(KParams kp, DevBufs d) {
   const int r = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= kp.ncell) return;
@@ -158,24 +168,29 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
   const int *start = d.cell_start + (size_t)r * (kp.ncell + 1);
   __shared__ float4 sx[32];
   __shared__ int sj[32];
-  __shared__ float4 sbc[8], sbh[8];    // cluster box centres and half extents
   const int cz = c % kp.nc[2], cy = (c / kp.nc[2]) % kp.nc[1], cx = c / (kp.nc[2] * kp.nc[1]);
   const int ib = start[c], ie = start[c + 1];
   const float3 Lbox = make_float3(kp.L[0], kp.L[1], kp.L[2]);
   const float3 Linv = make_float3(kp.invL[0], kp.invL[1], kp.invL[2]);
   const float rlist2 = kp.rlist2;
-  const float rlist2_pre = kp.rlist2 * 1.001f;
+  // band around r_list^2 inside which the fast (image-staged, rounding-different) d^2 may
+  // disagree with the canonical fp32 value; |delta d^2| < 1e-5 r_list^2 (R14)
+  const float lo2 = kp.rlist2 * (1.0f - 3e-5f), hi2 = kp.rlist2 * (1.0f + 3e-5f);
+  const bool fast = kp.ns[0] == 5 && kp.ns[1] == 5 && kp.ns[2] == 5;
   // stencil tables (cell index and, for +-2 stencils, the uniform periodic image shift
   // L * floor(raw / nc) of that j-cell; dimensions with < 5 cells use per-lane images)
   __shared__ int s_cell[3][8];
   __shared__ float s_wsh[3][8];
+  __shared__ int s_wi[3][8];
   if (lane < 24) {
     const int dd = lane >> 3, o = lane & 7;
     const int cdim = dd == 0 ? cx : (dd == 1 ? cy : cz);
     if (o < kp.ns[dd]) {
       const int raw = cdim + kp.so[dd] + o;
+      const int w = kp.ns[dd] == 5 ? (raw + kp.nc[dd]) / kp.nc[dd] - 1 : 0;
       s_cell[dd][o] = (raw + 2 * kp.nc[dd]) % kp.nc[dd];
-      s_wsh[dd][o] = kp.ns[dd] == 5 ? kp.L[dd] * (float)((raw + kp.nc[dd]) / kp.nc[dd] - 1) : 0.f;
+      s_wi[dd][o] = w;
+      s_wsh[dd][o] = kp.L[dd] * (float)w;
     }
   }
   __syncwarp();
@@ -197,73 +212,57 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
         for (int oz = 0; oz < kp.ns[2]; ++oz) {
           const int cc = (gx * kp.nc[1] + gy) * kp.nc[2] + s_cell[2][oz];
           const float wsz = s_wsh[2][oz];
+          // accepted pairs' canonical image k = -(j-cell shift) (nearest image, r < L/2)
+          const int fast_code = (1 - s_wi[0][ox]) * 9 + (1 - s_wi[1][oy]) * 3 + (1 - s_wi[2][oz]);
           const int jb = start[cc], je = start[cc + 1];
           for (int j0 = jb; j0 < je; j0 += 32) {
             const int nj = min(32, je - j0);
             __syncwarp();
             if (lane < nj) {
               const int j = j0 + lane;
-              sx[lane] = xq[j];
+              const float4 p = xq[j];
+              // fast path: stage the j-cell's periodic image (uniform for a +-2 stencil)
+              sx[lane] = fast ? make_float4(p.x + wsx, p.y + wsy, p.z + wsz, 0.f) : p;
               sj[lane] = j | ((meta[j].y & (int)kEntryTypeMask) << kEntryTypeShift);
             }
             __syncwarp();
-            // bounding box of each cluster of 4 consecutive staged atoms (z-sorted in the cell)
-            {
-              float4 p = sx[min(lane, nj - 1)];
-              float lo_x = p.x, lo_y = p.y, lo_z = p.z, hi_x = p.x, hi_y = p.y, hi_z = p.z;
-#pragma unroll
-              for (int o = 1; o < 4; o <<= 1) {
-                lo_x = fminf(lo_x, __shfl_xor_sync(0xffffffffu, lo_x, o));
-                lo_y = fminf(lo_y, __shfl_xor_sync(0xffffffffu, lo_y, o));
-                lo_z = fminf(lo_z, __shfl_xor_sync(0xffffffffu, lo_z, o));
-                hi_x = fmaxf(hi_x, __shfl_xor_sync(0xffffffffu, hi_x, o));
-                hi_y = fmaxf(hi_y, __shfl_xor_sync(0xffffffffu, hi_y, o));
-                hi_z = fmaxf(hi_z, __shfl_xor_sync(0xffffffffu, hi_z, o));
-              }
-              if ((lane & 3) == 0) {
-                sbc[lane >> 2] = make_float4(0.5f * (lo_x + hi_x) + wsx, 0.5f * (lo_y + hi_y) + wsy,
-                                             0.5f * (lo_z + hi_z) + wsz, 0.f);
-                sbh[lane >> 2] = make_float4(0.5f * (hi_x - lo_x), 0.5f * (hi_y - lo_y), 0.5f * (hi_z - lo_z), 0.f);
-              }
-              __syncwarp();
-            }
             if (!valid) continue;
-            // four candidates (one cluster) per pass (ILP); appends stay in candidate order
             for (int t0 = 0; t0 < nj; t0 += 4) {
-              // conservative prefilter: distance from x_i to the cluster box (nearest image);
-              // the box contains its atoms, so a rejected cluster cannot hold a list pair
-              // (margin 1e-3 relative on d^2 covers the float rounding of this estimate)
-              {
-                const float4 bc = sbc[t0 >> 2], bh = sbh[t0 >> 2];
-                float cx_ = bc.x - xi.x, cy_ = bc.y - xi.y, cz_ = bc.z - xi.z;
-                if (kp.ns[0] != 5) cx_ -= Lbox.x * rintf(cx_ * Linv.x);
-                if (kp.ns[1] != 5) cy_ -= Lbox.y * rintf(cy_ * Linv.y);
-                if (kp.ns[2] != 5) cz_ -= Lbox.z * rintf(cz_ * Linv.z);
-                const float gx_ = fmaxf(fabsf(cx_) - bh.x, 0.f), gy_ = fmaxf(fabsf(cy_) - bh.y, 0.f),
-                            gz_ = fmaxf(fabsf(cz_) - bh.z, 0.f);
-                if (gx_ * gx_ + gy_ * gy_ + gz_ * gz_ > rlist2_pre) continue;
-              }
               float d2v[4], kxv[4], kyv[4], kzv[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const float4 xj = sx[min(t0 + u, nj - 1)];
-                // canonical formula (R14): dx = x_j - x_i ; dx -= L rint(dx / L)
-                const float rx = __fsub_rn(xj.x, xi.x), ry = __fsub_rn(xj.y, xi.y), rz = __fsub_rn(xj.z, xi.z);
-                // positions are wrapped into [0, L] at the rebuild, so |dx / L| <= 1 and
-                // rint(t) == (t > 0.5) - (t < -0.5) exactly (ties to even); the selects run on
-                // the ALU pipe instead of the XU pipe FRND needs
-                kxv[u] = rint_unit(__fmul_rn(rx, Linv.x));
-                kyv[u] = rint_unit(__fmul_rn(ry, Linv.y));
-                kzv[u] = rint_unit(__fmul_rn(rz, Linv.z));
-                const float dx = __fsub_rn(rx, __fmul_rn(Lbox.x, kxv[u]));
-                const float dy = __fsub_rn(ry, __fmul_rn(Lbox.y, kyv[u]));
-                const float dz = __fsub_rn(rz, __fmul_rn(Lbox.z, kzv[u]));
-                d2v[u] = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+                if (fast) {
+                  // approximate d^2 from the staged image; exact canonical decision below
+                  // only for the rare candidates within the rounding band of r_list^2
+                  const float dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
+                  d2v[u] = dx * dx + dy * dy + dz * dz;
+                } else {
+                  // canonical formula (R14): dx = x_j - x_i ; dx -= L rint(dx / L);
+                  // positions are wrapped into [0, L] at the rebuild, so |dx / L| <= 1 and
+                  // rint(t) == (t > 0.5) - (t < -0.5) exactly (ties to even)
+                  const float rx = __fsub_rn(xj.x, xi.x), ry = __fsub_rn(xj.y, xi.y), rz = __fsub_rn(xj.z, xi.z);
+                  kxv[u] = rint_unit(__fmul_rn(rx, Linv.x));
+                  kyv[u] = rint_unit(__fmul_rn(ry, Linv.y));
+                  kzv[u] = rint_unit(__fmul_rn(rz, Linv.z));
+                  const float dx = __fsub_rn(rx, __fmul_rn(Lbox.x, kxv[u]));
+                  const float dy = __fsub_rn(ry, __fmul_rn(Lbox.y, kyv[u]));
+                  const float dz = __fsub_rn(rz, __fmul_rn(Lbox.z, kzv[u]));
+                  d2v[u] = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
+                }
               }
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                if (t0 + u >= nj || !(d2v[u] < rlist2)) continue;
-                const int code = (int)(kxv[u] * 9.0f + kyv[u] * 3.0f + kzv[u]) + 13;
+                if (t0 + u >= nj) continue;
+                int code;
+                if (fast) {
+                  if (d2v[u] >= hi2) continue;
+                  if (d2v[u] >= lo2 && !canonical_in(xq[sj[t0 + u] & (int)kEntryJMask], xi, Lbox, Linv, rlist2)) continue;
+                  code = fast_code;
+                } else {
+                  if (!(d2v[u] < rlist2)) continue;
+                  code = (int)(kxv[u] * 9.0f + kyv[u] * 3.0f + kzv[u]) + 13;
+                }
                 const int je_ = sj[t0 + u] | (code << kEntryImgShift);
                 const int j = je_ & (int)kEntryJMask;
                 if (j == i) continue;

@@ -94,6 +94,37 @@ def fit_curve(pH, x, hill=False, iters=200):
     return (float(p[0]), float(p[1])) if hill else float(p[0])
 
 
+TI_GRID = (-0.1, -0.05, 0.0, 0.05, 0.1, 0.2, 0.4, 0.6, 0.8, 0.9, 0.95, 1.0, 1.05, 1.1)
+
+
+def fit_vmm(kind, lp, lt, mean_dvdl, degree=5):
+    """Vmm coefficients c[a*6+b] from fixed-lambda TI means: fit the
+    derivatives of a degree-5 x degree-5 polynomial P (all mixing terms, constant gauge 0)
+    to <dV_coul/dlambda> at the grid points, both derivative blocks stacked, and return
+    Vmm = -P (dVmm/dlambda = -<dV_coul/dlambda>, R3).  kind 2: lp only."""
+    n = degree + 1
+    lp = np.asarray(lp, np.float64)
+    g = np.asarray(mean_dvdl, np.float64).reshape(len(lp), -1)
+    if int(kind) == 2:
+        powers = [(a, 0) for a in range(1, n)]
+        blocks = [np.stack([a * lp ** (a - 1) for a, _ in powers], 1)]
+        rhs = [g[:, 0]]
+    else:
+        lt = np.asarray(lt, np.float64)
+        powers = [(a, b) for a in range(n) for b in range(n) if a or b]
+        dp = np.stack([a * lp ** (a - 1) * lt ** b if a else 0.0 * lp for a, b in powers], 1)
+        dt = np.stack([b * lp ** a * lt ** (b - 1) if b else 0.0 * lt for a, b in powers], 1)
+        blocks, rhs = [dp, dt], [g[:, 0], g[:, 1]]
+    A = np.concatenate(blocks, 0)
+    y = np.concatenate(rhs)
+    q, rr = np.linalg.qr(A)
+    coef = np.linalg.solve(rr, q.T @ y)
+    out = np.zeros(n * n)
+    for (a, b), v in zip(powers, coef):
+        out[a * n + b] = -v
+    return out
+
+
 def bootstrap(pH_levels, fractions, B=5000, seed=0, hill=False):
     """fractions [n_pH, R]: resample R replica fractions per pH with replacement, refit,
     95% percentile interval."""

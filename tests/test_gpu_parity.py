@@ -172,16 +172,24 @@ def test_fixed_lambda_ti_mode(cph):
     instantaneous dV/dlambda."""
     s = small_system()
     lam = np.array([[0.2, 0.4, 0.9]])
-    ctx = cph.cph_create(s, [4.4], [5], lambda0=lam, mode=1)
+    vel = make_velocities(s, 9)
+    ctx = cph.cph_create(s, [4.4], [5], lambda0=lam, mode=1, vel_replicas=vel[None])
+    ref = OracleReplica(s, 4.4, 5, lam0=lam[0], vel0=vel, fixed_lambda=True)
     acc = np.zeros(s.n_coords)
+    acc_ref = np.zeros(s.n_coords)
     for _ in range(6):
         ctx.cph_step(1)
+        ref.step()
         c, b = ctx.cph_get_dvdl(0)
-        acc += c + b
+        acc += c
+        acc_ref += ref.cur["dvdl_coul"]
         np.testing.assert_array_equal(ctx.cph_get_lambdas(0)[0], lam[0])
     mean, n = ctx.cph_get_ti_means(0)
     assert n == 6
     np.testing.assert_allclose(mean, acc / 6, rtol=1e-12, atol=1e-12)
+    # same Philox streams: the oracle's TI mean over the same 6 steps agrees
+    scale = np.maximum(np.abs(acc_ref / 6), ref.cur["term_mag"])
+    assert np.all(np.abs(mean - acc_ref / 6) <= 1e-4 * scale), (mean, acc_ref / 6)
 
 
 def test_gpu_sampling_follows_hh_when_coulomb_dvdl_vanishes(cph):

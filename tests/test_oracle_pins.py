@@ -461,3 +461,30 @@ def test_baoab_conserves_energy_without_friction():
         r.step()
         drift.append(r.energies()["total"] - E0)
     assert np.max(np.abs(drift)) < 2e-4 * ke
+
+
+# --------------------------------------------------------------------------- calibration (a11)
+def test_ti_grid_is_the_si_list():
+    from oracle.calibration import TI_GRID
+    assert len(TI_GRID) == 14 and len(TI_GRID) ** 2 == 196          # P:8
+
+
+def test_vmm_fit_recovers_exact_polynomial_and_flattens():
+    """SPEC S:201 (exact degree-5 reference recovered to 1e-8) and S:203 (flattening:
+    Vmm + U_ref has zero gradient)."""
+    from oracle.calibration import TI_GRID, vmm_from_ti
+    rng = np.random.default_rng(4)
+    c_ref = rng.normal(size=36)
+    c_ref[0] = 0.0
+    LP, LT = np.meshgrid(TI_GRID, TI_GRID, indexing="ij")
+    lp, lt = LP.ravel(), LT.ravel()
+    g = np.array([bias.vmm(c_ref, a, b)[1:] for a, b in zip(lp, lt)])   # dU/dlp, dU/dlt
+    vm = vmm_from_ti(3, lp, lt, g)
+    np.testing.assert_allclose(vm, -c_ref, atol=1e-8)
+    for a, b in rng.uniform(-0.1, 1.1, (20, 2)):
+        _, gp, gt = bias.vmm(vm + c_ref, a, b)
+        assert abs(gp) < 1e-7 and abs(gt) < 1e-7
+    c1 = np.zeros(36)
+    c1[[6, 12, 18, 24, 30]] = rng.normal(size=5)
+    g1 = np.array([[bias.vmm(c1, a, 0.0)[1]] for a in TI_GRID])
+    np.testing.assert_allclose(vmm_from_ti(2, np.array(TI_GRID), None, g1), -c1, atol=1e-8)

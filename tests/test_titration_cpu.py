@@ -69,3 +69,18 @@ def test_bootstrap_interval_contains_truth():
     assert lo <= 4.5 <= hi and hi - lo < 0.2
     with pytest.raises(ValueError):
         T.fit_curve([1.0, 2.0], [1.0, 1.0])
+
+
+def test_fit_vmm_matches_oracle_fit():
+    from oracle import bias as OB
+    from oracle.calibration import vmm_from_ti
+    rng = np.random.default_rng(8)
+    c = rng.normal(size=36)
+    c[0] = 0.0
+    LP, LT = np.meshgrid(T.TI_GRID, T.TI_GRID, indexing="ij")
+    lp, lt = LP.ravel(), LT.ravel()
+    g = np.array([OB.vmm(c, a, b)[1:] for a, b in zip(lp, lt)]) + rng.normal(0, 0.1, (lp.size, 2))
+    np.testing.assert_allclose(T.fit_vmm(3, lp, lt, g), vmm_from_ti(3, lp, lt, g), atol=1e-9)
+    g1 = g[:14, :1]
+    x = np.array(T.TI_GRID)
+    np.testing.assert_allclose(T.fit_vmm(2, x, None, g1), vmm_from_ti(2, x, None, g1), atol=1e-9)
