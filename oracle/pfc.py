@@ -38,11 +38,23 @@ def free_energy_1d(h, d1, g, T, kw):
     return -kT(T) * math.log(zd / zp)
 
 
+D1_BOUND = 80.0     # kJ/mol; reading R22: the correction saturates at +-80 when unreachable
+
+
+def _root_or_bound(fn, lo=-D1_BOUND, hi=D1_BOUND):
+    """Root of an increasing function on [lo, hi]; if none, the bound nearer to it (R22)."""
+    flo, fhi = fn(lo), fn(hi)
+    if flo > 0:
+        return lo
+    if fhi < 0:
+        return hi
+    return optimize.brentq(fn, lo, hi, xtol=1e-13, rtol=1e-15, maxiter=500)
+
+
 def pfc_2state(h, pKa, pH, T, kw):
-    """d1 such that G_deprot - G_prot = ln10 kT (pKa - pH)."""
+    """d1 such that G_deprot - G_prot = ln10 kT (pKa - pH) (saturating, R22)."""
     target = delta_g(pKa, pH, T)
-    fn = lambda d1: free_energy_1d(h, d1, target, T, kw) - target
-    return optimize.brentq(fn, -60.0, 60.0, xtol=1e-13, rtol=1e-15, maxiter=500)
+    return _root_or_bound(lambda d1: free_energy_1d(h, d1, target, T, kw) - target)
 
 
 def _gl_nodes(breaks, sub=8, order=24):
@@ -85,4 +97,20 @@ def pfc_3state(h, pKa3, pH, T, kw):
         a, b = quadrant_free_energies(h, v[0], v[1], pKa3, pH, T, kw)
         return [a - gd, b - ge]
     sol = optimize.root(res, [0.0, 0.0], method="hybr", tol=1e-14)
-    return float(sol.x[0]), float(sol.x[1])
+    if sol.success and np.max(np.abs(res(sol.x))) < 1e-9 and np.all(np.abs(sol.x) <= D1_BOUND):
+        return float(sol.x[0]), float(sol.x[1])
+    # unreachable targets (R22): nested saturating bisection - the tautomer split
+    # G_eps - G_delta = dG_eps - dG_delta for d1_t inside, the macro deprotonation free
+    # energy -kT ln(e^{-b dG_delta} + e^{-b dG_eps}) for d1_p outside
+    kt = kT(T)
+    macro = -kt * math.log(math.exp(-gd / kt) + math.exp(-ge / kt))
+
+    def inner(d1p):
+        return _root_or_bound(lambda d1t: np.subtract(*quadrant_free_energies(h, d1p, d1t, pKa3, pH, T, kw)[::-1])
+                              - (ge - gd))
+
+    def outer(d1p):
+        a, b = quadrant_free_energies(h, d1p, inner(d1p), pKa3, pH, T, kw)
+        return -kt * math.log(math.exp(-a / kt) + math.exp(-b / kt)) - macro
+    d1p = _root_or_bound(outer)
+    return float(d1p), float(inner(d1p))

@@ -3,7 +3,8 @@
 // Z_prot = int_{lp<0.5} e^{-beta V}, Z_deprot = int_{lp>=0.5} e^{-beta V} over the whole
 // wall-bounded range, V = Vdw + VpH (Vmm excluded).  The lambda=1 well depth d1
 // is solved so that G_deprot - G_prot = ln10 kT (pKa - pH) (bisection); His-like sites solve
-// (d1_p, d1_t) for the two micro free energies (Newton).  Composite Gauss-Legendre quadrature
+// (d1_p, d1_t) for the two micro free energies (Newton).  Targets out of reach of the single
+// well-depth correction saturate at +-80 kJ/mol (R22).  Composite Gauss-Legendre quadrature
 // with panels split at the spline knots and wall onsets, where the integrand is analytic.
 #include <cmath>
 #include <string>
@@ -83,29 +84,33 @@ double free_energy_2state(const Nodes &nd, double h, double d1, double g, double
 
 double delta_g(double pKa, double pH, double T) { return kLn10 * kBoltz * T * (pKa - pH); }
 
+// DESIGN.md R22: root of an increasing function on [-80, 80] kJ/mol, or the bound nearer
+// to it when the target is out of reach of the single well-depth correction
+constexpr double kD1Bound = 80.0;
+template <class F>
+double root_or_bound(F f) {
+  double lo = -kD1Bound, hi = kD1Bound;
+  if (f(lo) > 0.0) return lo;
+  if (f(hi) < 0.0) return hi;
+  for (int it = 0; it < 200 && hi - lo > 1e-13; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (f(mid) < 0.0) lo = mid; else hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
 bool pfc_two_state(double h, double pKa, double pH, double T, double kw, double *d1, std::string *err) {
   static const Nodes nd = make_nodes(12, 24);
   const double kT = kBoltz * T;
   const double target = delta_g(pKa, pH, T);
-  double lo = -80.0, hi = 80.0;
-  double flo = free_energy_2state(nd, h, lo, target, kT, kw) - target;
-  double fhi = free_energy_2state(nd, h, hi, target, kT, kw) - target;
-  if (!(flo < 0.0 && fhi > 0.0)) {
-    if (err) *err = "PFC: target free energy not bracketed by well depths in [-80, 80] kJ/mol";
-    return false;
-  }
-  for (int it = 0; it < 200 && hi - lo > 1e-13; ++it) {
-    const double mid = 0.5 * (lo + hi);
-    const double fm = free_energy_2state(nd, h, mid, target, kT, kw) - target;
-    if (fm < 0.0) lo = mid; else hi = mid;
-  }
-  *d1 = 0.5 * (lo + hi);
+  *d1 = root_or_bound([&](double x) { return free_energy_2state(nd, h, x, target, kT, kw) - target; });
+  (void)err;
   return true;
 }
 
 bool pfc_three_state(double h, const double pKa3[3], double pH, double T, double kw, double *d1p,
                      double *d1t, std::string *err) {
-  static const Nodes nd = make_nodes(6, 20);
+  static const Nodes nd = make_nodes(3, 20);
   const int n = (int)nd.x.size();
   const double kT = kBoltz * T;
   const double gd = delta_g(pKa3[1], pH, T), ge = delta_g(pKa3[2], pH, T);
@@ -148,10 +153,7 @@ bool pfc_three_state(double h, const double pKa3[3], double pH, double T, double
     const double j00 = (fa[0] - f[0]) / e, j10 = (fa[1] - f[1]) / e;
     const double j01 = (fb[0] - f[0]) / e, j11 = (fb[1] - f[1]) / e;
     const double det = j00 * j11 - j01 * j10;
-    if (!(std::fabs(det) > 1e-300)) {
-      if (err) *err = "PFC (3-state): singular Jacobian";
-      return false;
-    }
+    if (!(std::fabs(det) > 1e-300)) break;      // unreachable / degenerate: fall back below
     double s0 = (j11 * f[0] - j01 * f[1]) / det;
     double s1 = (-j10 * f[0] + j00 * f[1]) / det;
     const double mx = std::fmax(std::fabs(s0), std::fabs(s1));
@@ -161,12 +163,31 @@ bool pfc_three_state(double h, const double pKa3[3], double pH, double T, double
   }
   double f[2];
   quad(x0, x1, f);
-  if (!(std::fabs(f[0]) < 1e-9 && std::fabs(f[1]) < 1e-9)) {
-    if (err) *err = "PFC (3-state): Newton iteration did not converge";
-    return false;
+  if (std::fabs(f[0]) < 1e-9 && std::fabs(f[1]) < 1e-9 && std::fabs(x0) <= kD1Bound && std::fabs(x1) <= kD1Bound) {
+    *d1p = x0;
+    *d1t = x1;
+    return true;
   }
-  *d1p = x0;
-  *d1t = x1;
+  // R22: unreachable targets -> nested saturating bisection: the tautomer split
+  // G_eps - G_delta = dG_eps - dG_delta for d1_t inside, the macro deprotonation free
+  // energy -kT ln(e^{-b dG_delta} + e^{-b dG_eps}) for d1_p outside
+  const double macro = -kT * std::log(std::exp(-gd / kT) + std::exp(-ge / kT));
+  auto inner = [&](double dp) {
+    return root_or_bound([&](double dt) {
+      double q[2];
+      quad(dp, dt, q);
+      return (q[1] + ge) - (q[0] + gd) - (ge - gd);
+    });
+  };
+  auto outer = [&](double dp) {
+    double q[2];
+    quad(dp, inner(dp), q);
+    const double a = q[0] + gd, b = q[1] + ge;
+    return -kT * std::log(std::exp(-a / kT) + std::exp(-b / kT)) - macro;
+  };
+  *d1p = root_or_bound(outer);
+  *d1t = inner(*d1p);
+  (void)err;
   return true;
 }
 

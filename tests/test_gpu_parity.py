@@ -285,3 +285,13 @@ def test_full_size_c5_sampled_parity(cph):
     err = np.abs(coul - ref) / np.maximum(np.abs(ref), mag)
     print("C5 dvdl max rel", err.max())
     assert err.max() < 2e-5
+
+
+def test_pfc_saturation_matches_oracle(cph):
+    """Reading R22 at the extreme pH of the lysozyme/cardiotoxin grids."""
+    s = make_system(2)
+    pH = np.array([-1.0, 1.0, 9.0])
+    ctx = cph.cph_create(s, pH, replica_seeds(3, 3))
+    for r in range(3):
+        ref = [OPFC.pfc_2state(6.0, s.pKa[0, 0], pH[r], 300.0, 1e6), *OPFC.pfc_3state(6.0, s.pKa[1], pH[r], 300.0, 1e6)]
+        np.testing.assert_allclose(ctx.cph_get_bias_params(r), ref, atol=1e-7)

@@ -488,3 +488,17 @@ def test_vmm_fit_recovers_exact_polynomial_and_flattens():
     c1[[6, 12, 18, 24, 30]] = rng.normal(size=5)
     g1 = np.array([[bias.vmm(c1, a, 0.0)[1]] for a in TI_GRID])
     np.testing.assert_allclose(vmm_from_ti(2, np.array(TI_GRID), None, g1), -c1, atol=1e-8)
+
+
+def test_pfc_saturates_when_target_unreachable():
+    """Reading R22: |pH - pKa| beyond ~3.7 on the protonated side cannot be corrected by d1
+    alone at h = 6 (the deprotonated half contains the barrier top); d1 saturates at +80 and the
+    deprotonated population is then below the H-H value by a negligible amount."""
+    assert pfc.pfc_2state(6.0, 4.0, -1.0, 300.0, 1e6) == pfc.D1_BOUND
+    d1 = pfc.pfc_2state(6.0, 4.0, 0.2, 300.0, 1e6)
+    assert 0 < d1 < pfc.D1_BOUND
+    x = np.linspace(-0.45, 1.45, 200001)
+    V = bias.vdw(x, 6.0, 0.0, pfc.D1_BOUND, 1e6)[0] + x * bias.delta_g(4.0, -1.0, 300.0)
+    w = np.exp(-(V - V.min()) / kT(300.0))
+    frac = w[x >= 0.5].sum() / w.sum()
+    assert frac < 1e-3 and 1.0 / (10 ** 5 + 1) < frac
