@@ -51,15 +51,20 @@ struct Nodes {
   std::vector<double> x, w;
 };
 
+// Panels end at the spline knots and wall onsets (the integrand is analytic inside); the
+// steep quartic-wall intervals get more sub-panels.  Beyond -0.35 / 1.35 the integrand is
+// below 1e-30 of its peak.
 Nodes make_nodes(int sub, int order) {
-  static const double brk[] = {-0.5, -0.1, 0.0, 0.5, 1.0, 1.1, 1.5};
+  static const double brk[] = {-0.35, -0.1, 0.0, 0.5, 1.0, 1.1, 1.35};
+  static const int wsub[] = {3, 1, 2, 2, 1, 3};
   std::vector<double> gx, gw;
   gauss_legendre(order, gx, gw);
   Nodes nd;
   for (int b = 0; b + 1 < (int)(sizeof(brk) / sizeof(brk[0])); ++b) {
     const double a0 = brk[b], a1 = brk[b + 1];
-    for (int s = 0; s < sub; ++s) {
-      const double c = a0 + (a1 - a0) * s / sub, e = a0 + (a1 - a0) * (s + 1) / sub;
+    const int nsub = sub * wsub[b];
+    for (int s = 0; s < nsub; ++s) {
+      const double c = a0 + (a1 - a0) * s / nsub, e = a0 + (a1 - a0) * (s + 1) / nsub;
       for (int k = 0; k < order; ++k) {
         nd.x.push_back(0.5 * (e - c) * gx[k] + 0.5 * (e + c));
         nd.w.push_back(0.5 * (e - c) * gw[k]);
@@ -100,7 +105,7 @@ double root_or_bound(F f) {
 }
 
 bool pfc_two_state(double h, double pKa, double pH, double T, double kw, double *d1, std::string *err) {
-  static const Nodes nd = make_nodes(12, 24);
+  static const Nodes nd = make_nodes(6, 24);
   const double kT = kBoltz * T;
   const double target = delta_g(pKa, pH, T);
   *d1 = root_or_bound([&](double x) { return free_energy_2state(nd, h, x, target, kT, kw) - target; });
@@ -110,7 +115,7 @@ bool pfc_two_state(double h, double pKa, double pH, double T, double kw, double 
 
 bool pfc_three_state(double h, const double pKa3[3], double pH, double T, double kw, double *d1p,
                      double *d1t, std::string *err) {
-  static const Nodes nd = make_nodes(3, 20);
+  static const Nodes nd = make_nodes(2, 20);
   const int n = (int)nd.x.size();
   const double kT = kBoltz * T;
   const double gd = delta_g(pKa3[1], pH, T), ge = delta_g(pKa3[2], pH, T);
