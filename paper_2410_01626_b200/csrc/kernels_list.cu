@@ -159,6 +159,10 @@ __global__ void k_copy_back(KParams kp, DevBufs d) {
 // One warp per cell: the i atoms are the cell's atoms (one per lane, chunks of 32), and every
 // stencil cell's atoms are staged through shared memory (coalesced loads, broadcast reads),
 // so the loop structure is uniform across the warp.
+// padding of the geometric cell bounds and of the z-window radius (nm): >> the fp32
+// rounding of wrapped positions (|x| <= L ~ 14 nm, ulp ~ 1e-6)
+constexpr float kWinPad = 1e-4f;
+
 __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
   const int r = blockIdx.y, c = blockIdx.x;
   const int lane = threadIdx.x;
@@ -177,6 +181,9 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
   // disagree with the canonical fp32 value; |delta d^2| < 1e-5 r_list^2 (R14)
   const float lo2 = kp.rlist2 * (1.0f - 3e-5f), hi2 = kp.rlist2 * (1.0f + 3e-5f);
   const bool fast = kp.ns[0] == 5 && kp.ns[1] == 5 && kp.ns[2] == 5;
+  const float csx = kp.L[0] / (float)kp.nc[0], csy = kp.L[1] / (float)kp.nc[1], csz = kp.L[2] / (float)kp.nc[2];
+  const float win_r = sqrtf(kp.rlist2) * 1.0001f + kWinPad;
+  const float win_r2 = win_r * win_r;
   // stencil tables (cell index and, for +-2 stencils, the uniform periodic image shift
   // L * floor(raw / nc) of that j-cell; dimensions with < 5 cells use per-lane images)
   __shared__ int s_cell[3][8];
@@ -209,7 +216,35 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
       for (int oy = 0; oy < kp.ns[1]; ++oy) {
         const int gy = s_cell[1][oy];
         const float wsy = s_wsh[1][oy];
+        // fast path: z window of this stencil column.  Each lane's reach in z is
+        // sqrt(R^2 - dxy^2), dxy its xy distance to the column (geometric cell bounds in the
+        // staged image frame, padded); the warp tests only the staged atoms whose z lies in
+        // the union of the lanes' windows (cells are z-sorted, so that is a contiguous slice).
+        // R and the pads are far outside the fp32 rounding of d^2, so no accepted pair is cut.
+        float zlo = -INFINITY, zhi = INFINITY;
+        if (fast) {
+          const float xlo = (float)(cx - 2 + ox) * csx - kWinPad, xhi = xlo + csx + 2.f * kWinPad;
+          const float ylo = (float)(cy - 2 + oy) * csy - kWinPad, yhi = ylo + csy + 2.f * kWinPad;
+          const float ddx = fmaxf(0.f, fmaxf(xlo - xi.x, xi.x - xhi));
+          const float ddy = fmaxf(0.f, fmaxf(ylo - xi.y, xi.y - yhi));
+          const float rr2 = win_r2 - ddx * ddx - ddy * ddy;
+          zlo = INFINITY; zhi = -INFINITY;
+          if (valid && rr2 > 0.f) {
+            const float rr = sqrtf(rr2);
+            zlo = xi.z - rr; zhi = xi.z + rr;
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
+            zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
+          }
+          if (!(zlo <= zhi)) continue;   // no lane reaches this column (warp-uniform)
+        }
         for (int oz = 0; oz < kp.ns[2]; ++oz) {
+          if (fast) {
+            const float zc = (float)(cz - 2 + oz) * csz;
+            if (zhi < zc - kWinPad || zlo > zc + csz + kWinPad) continue;
+          }
           const int cc = (gx * kp.nc[1] + gy) * kp.nc[2] + s_cell[2][oz];
           const float wsz = s_wsh[2][oz];
           // accepted pairs' canonical image k = -(j-cell shift) (nearest image, r < L/2)
@@ -217,21 +252,30 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
           const int jb = start[cc], je = start[cc + 1];
           for (int j0 = jb; j0 < je; j0 += 32) {
             const int nj = min(32, je - j0);
+            int tb = 0, te = nj;
             __syncwarp();
-            if (lane < nj) {
-              const int j = j0 + lane;
-              const float4 p = xq[j];
-              // fast path: stage the j-cell's periodic image (uniform for a +-2 stencil)
-              sx[lane] = fast ? make_float4(p.x + wsx, p.y + wsy, p.z + wsz, 0.f) : p;
-              sj[lane] = j | ((meta[j].y & (int)kEntryTypeMask) << kEntryTypeShift);
+            {
+              float zt = 0.f;
+              if (lane < nj) {
+                const int j = j0 + lane;
+                const float4 p = xq[j];
+                // fast path: stage the j-cell's periodic image (uniform for a +-2 stencil)
+                sx[lane] = fast ? make_float4(p.x + wsx, p.y + wsy, p.z + wsz, 0.f) : p;
+                sj[lane] = j | ((meta[j].y & (int)kEntryTypeMask) << kEntryTypeShift);
+                zt = p.z + wsz;
+              }
+              if (fast) {
+                tb = __popc(__ballot_sync(0xffffffffu, lane < nj && zt < zlo));
+                te = __popc(__ballot_sync(0xffffffffu, lane < nj && zt <= zhi));
+              }
             }
             __syncwarp();
             if (!valid) continue;
-            for (int t0 = 0; t0 < nj; t0 += 4) {
+            for (int t0 = tb; t0 < te; t0 += 4) {
               float d2v[4], kxv[4], kyv[4], kzv[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                const float4 xj = sx[min(t0 + u, nj - 1)];
+                const float4 xj = sx[min(t0 + u, te - 1)];
                 if (fast) {
                   // approximate d^2 from the staged image; exact canonical decision below
                   // only for the rare candidates within the rounding band of r_list^2
@@ -253,7 +297,7 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
               }
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                if (t0 + u >= nj) continue;
+                if (t0 + u >= te) continue;
                 int code;
                 if (fast) {
                   if (d2v[u] >= hi2) continue;
