@@ -12,12 +12,17 @@ Follows, in order:
     Atoms: m from the system, mass 0 = frozen.  lambda: m = 60 u,
     gamma = 1/tau = 1 ps^-1.  Noise from oracle.philox.
   * Partition Function Correction at construction.
+  * Optional DBO (oracle.dbo, PAPER.md:764-805): statistics after every completed step;
+    at the end of a block step S the rules run, the PFC is recomputed for the adjusted
+    sites and the forces are re-evaluated at the unchanged (x, lambda),
+    so step S+1 starts on the new bias.
 """
 import math
 
 import numpy as np
 
 from . import bias as B
+from . import dbo as DBO
 from . import pfc as PFC
 from .charges import charges, coord_ptr
 from .ewald import (ewald_beta, exclusion_correction, net_charge_term, real_space,
@@ -31,7 +36,7 @@ ENERGY_TERMS = ("LJ", "real", "excl", "self", "recip", "net", "bias", "KE_atoms"
 
 class OracleReplica:
     def __init__(self, sys, pH, seed, lam0=None, vel0=None, pos0=None, params=None,
-                 recip="pme", nmax=None, fixed_lambda=False):
+                 recip="pme", nmax=None, fixed_lambda=False, dbo=None, dbo_params=None):
         self.sys = sys
         p = dict(sys.params)
         if params:
@@ -55,6 +60,20 @@ class OracleReplica:
         self.lam = np.zeros(C) if lam0 is None else np.asarray(lam0, np.float64).copy()
         self.lamv = np.zeros(C)
         self.step_index = 0
+        # DBO: per-coordinate (a0, a1, h_prot, h_deprot); config keys well, barrier (bool),
+        # well_steps, barrier_steps, censor_steps
+        self.dbo = dict(well=False, barrier=False, well_steps=20000, barrier_steps=500000, censor_steps=5000)
+        if dbo:
+            self.dbo.update(dbo)
+        self.dbo_params = B.default_dbo(p["barrier"], C) if dbo_params is None else np.array(dbo_params, np.float64)
+        self.lp_of = np.full(C, -1)
+        for g, kind in enumerate(sys.group_kind):
+            if int(kind) == 3:
+                self.lp_of[self.cptr[g] + 1] = self.cptr[g]
+        self.stats_well = DBO.BlockStats(C)
+        self.stats_barrier = DBO.BlockStats(C)
+        self.events = []              # (step, coord, kind, old, new)
+        self.censor = []              # (group, step S): frames S < t <= S + censor_steps
         self.set_pH(pH)
         self.cur = self.evaluate(self.x, self.lam)
 
@@ -63,13 +82,44 @@ class OracleReplica:
         p = self.p
         self.pH = float(pH)
         self.d1 = np.zeros(int(self.cptr[-1]))
-        for g, kind in enumerate(self.sys.group_kind):
-            c0 = self.cptr[g]
-            if int(kind) == 2:
-                self.d1[c0] = PFC.pfc_2state(p["barrier"], self.sys.pKa[g, 0], pH, p["temperature"], p["wall_k"])
-            else:
-                self.d1[c0], self.d1[c0 + 1] = PFC.pfc_3state(p["barrier"], self.sys.pKa[g], pH,
-                                                              p["temperature"], p["wall_k"])
+        for g in range(len(self.sys.group_kind)):
+            self._pfc_group(g)
+
+    def _pfc_group(self, g):
+        p = self.p
+        c0 = self.cptr[g]
+        db = self.dbo_params
+        if int(self.sys.group_kind[g]) == 2:
+            self.d1[c0] = PFC.pfc_2state(db[c0, 2], self.sys.pKa[g, 0], self.pH, p["temperature"], p["wall_k"],
+                                         db[c0, 0], db[c0, 1])
+        else:
+            self.d1[c0], self.d1[c0 + 1] = PFC.pfc_3state(db[c0, 2], self.sys.pKa[g], self.pH, p["temperature"],
+                                                          p["wall_k"], db[c0:c0 + 2])
+
+    def set_dbo_params(self, dbo_params):
+        """Replace the DBO parameters, recompute the PFC and the forces."""
+        self.dbo_params = np.array(dbo_params, np.float64)
+        self.set_pH(self.pH)
+        self.cur = self.evaluate(self.x, self.lam)
+
+    def _dbo_block_end(self):
+        S = self.step_index
+        ev = []
+        if self.dbo["well"] and S % self.dbo["well_steps"] == 0:
+            ev += DBO.well_update(self.dbo_params, self.stats_well)
+            self.stats_well = DBO.BlockStats(len(self.lam))
+        if self.dbo["barrier"] and S % self.dbo["barrier_steps"] == 0:
+            ev += DBO.barrier_update(self.dbo_params, self.stats_barrier, self.lp_of)
+            self.stats_barrier = DBO.BlockStats(len(self.lam))
+        if not ev:
+            return
+        groups = sorted({int(np.searchsorted(self.cptr, c, side="right") - 1) for c, *_ in ev})
+        for c, kind, old, new in ev:
+            self.events.append((S, c, kind, old, new))
+        for g in groups:
+            self._pfc_group(g)
+            self.censor.append((g, S))
+        self.cur = self.evaluate(self.x, self.lam)
 
     def bias(self, lam):
         p = self.p
@@ -80,8 +130,10 @@ class OracleReplica:
             lp = lam[c0]
             lt = lam[c0 + 1] if int(kind) == 3 else 0.0
             d1t = self.d1[c0 + 1] if int(kind) == 3 else 0.0
+            nc = 2 if int(kind) == 3 else 1
             v, dp, dt = B.group_bias(kind, self.sys.vmm[g], self.sys.pKa[g], self.pH, p["temperature"],
-                                     p["barrier"], self.d1[c0], d1t, p["wall_k"], lp, lt)
+                                     p["barrier"], self.d1[c0], d1t, p["wall_k"], lp, lt,
+                                     self.dbo_params[c0:c0 + nc])
             E += v
             dv[c0] += dp
             if int(kind) == 3:
@@ -161,3 +213,7 @@ class OracleReplica:
             lamv = lamv + 0.5 * h * (-(cur["dvdl_coul"] + cur["dvdl_bias"])) / p["lambda_mass"]
         self.x, self.v, self.lam, self.lamv, self.cur = x, v, lam, lamv, cur
         self.step_index = n + 1
+        if not self.fixed_lambda and (self.dbo["well"] or self.dbo["barrier"]):
+            self.stats_well.add(self.lam, self.lp_of)
+            self.stats_barrier.add(self.lam, self.lp_of)
+            self._dbo_block_end()
