@@ -17,6 +17,9 @@
  *       (m_lambda = 60 u), dt = 2 fs, 300 K.
  *   a10 Partition Function Correction of the double-well depths at cph_create /
  *       cph_set_pH.
+ *   f1  optional Dynamic Barrier and Well Optimization with censoring
+ *       (R23-R26): per-step block statistics on the
+ *       device, controller rules and PFC refresh on the host at block ends.
  *
  * Conventions
  *   Units: nm, ps, u, kJ/mol, e, K.  lambda = 0 is protonated; a frame is
@@ -51,7 +54,7 @@
 extern "C" {
 #endif
 
-#define CPH_ABI_VERSION 1
+#define CPH_ABI_VERSION 2
 
 typedef struct cph_ctx cph_ctx;
 
@@ -132,7 +135,42 @@ typedef struct {
   void *(*dev_alloc)(size_t bytes, void *alloc_ctx);   /* NULL -> cudaMalloc */
   void (*dev_free)(void *ptr, void *alloc_ctx);
   void *alloc_ctx;
+  /* Dynamic Barrier and Well Optimization.  Both off by default;
+   * each can be enabled independently.  Block lengths must be
+   * multiples of nstlist.  The rule constants default to the paper's values. */
+  int32_t dbo_well;             /* 1: regulate the well centres */
+  int32_t dbo_barrier;          /* 1: regulate the barrier heights */
+  int64_t dbo_well_steps;       /* well block, steps (20000 = 40 ps) */
+  int64_t dbo_barrier_steps;    /* barrier block, steps (500000 = 1 ns) */
+  int64_t dbo_censor_steps;     /* censor window after an adjustment (5000 = 10 ps) */
+  double dbo_well_near;         /* 0.2: lambda < 0.2 near well 0, lambda > 1 - 0.2 near well 1 */
+  double dbo_residency;         /* 0.70: fraction of the block near one well to act */
+  double dbo_well_tol;          /* 0.03: |mean - ideal| tolerance */
+  double dbo_well_gain;         /* 0.5: shift = gain * (ideal - mean) */
+  double dbo_well_cap;          /* 0.08: |accumulated shift| cap */
+  double dbo_trans_lo;          /* 0.2 \  in transition: trans_lo < lambda < trans_hi */
+  double dbo_trans_hi;          /* 0.8 /                                           */
+  double dbo_target;            /* 0.25: target in-transition fraction */
+  double dbo_target_tol;        /* 0.05 */
+  double dbo_barrier_step;      /* 1.0 kJ/mol */
+  double dbo_barrier_min;       /* 1 kJ/mol */
+  double dbo_barrier_max;       /* 20 kJ/mol */
 } cph_params;
+
+/* DBO event kinds (cph_dbo_event.kind) */
+enum {
+  CPH_DBO_WELL0 = 0,            /* centre of the lambda = 0 well moved */
+  CPH_DBO_WELL1 = 1,            /* centre of the lambda = 1 well moved */
+  CPH_DBO_BARRIER = 2,          /* barrier of a lambda_p coordinate */
+  CPH_DBO_BARRIER_T_PROT = 3,   /* tautomer barrier used while protonated (lambda_p < 0.5) */
+  CPH_DBO_BARRIER_T_DEPROT = 4  /* tautomer barrier used while deprotonated */
+};
+
+typedef struct {
+  int64_t step;                 /* block-end step S; the new value applies from step S+1 */
+  int32_t replica, coord, kind, pad;
+  double old_value, new_value;  /* well centre (nm-free lambda units) or barrier kJ/mol */
+} cph_dbo_event;
 
 /* Fill *p with the defaults quoted above (pH/seed pointers NULL). */
 void cph_default_params(cph_params *p);
@@ -176,6 +214,33 @@ cph_status cph_get_bias_params(cph_ctx *ctx, int32_t replica, double *d1 /*[C]*/
  * dropped oldest-first and *n_dropped reports how many. */
 cph_status cph_get_frames(cph_ctx *ctx, int32_t replica, float *buf, int64_t cap,
                           int64_t *n_frames, int64_t *n_dropped);
+/* As cph_get_frames, plus per frame the step it was taken at (steps [cap] or NULL)
+ * and per frame and coordinate a censor flag (censored [cap*C] or NULL): 1 iff the
+ * coordinate's site had a DBO adjustment at a block end S with
+ * S < step <= S + dbo_censor_steps (R26). */
+cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t replica, float *buf, uint8_t *censored,
+                             int64_t *steps, int64_t cap, int64_t *n_frames, int64_t *n_dropped);
+/* DBO parameters per coordinate [C*4]: (a0, a1, h_prot, h_deprot) = well centres of
+ * the lambda = 0 and lambda = 1 wells, and the barrier heights (kJ/mol).  lambda_p
+ * coordinates use h_prot == h_deprot; a tautomer coordinate's barrier is
+ * h_prot + (h_deprot - h_prot) S(lambda_p), S the clamped smoothstep (R25).
+ * Before any adjustment: (0, 1, barrier, barrier). */
+cph_status cph_get_dbo_params(cph_ctx *ctx, int32_t replica, double *p);
+/* Replace them (e.g. a restart): requires |a0| <= 0.2, |a1 - 1| <= 0.2, barriers in
+ * (0, 100] and h_prot == h_deprot for lambda_p coordinates (else CPH_E_INVALID).
+ * Re-runs the PFC of that replica and re-evaluates its forces; block accumulators
+ * are kept. */
+cph_status cph_set_dbo_params(cph_ctx *ctx, int32_t replica, const double *p);
+/* Adjustment log since the last call (drained); *n = events written, up to cap;
+ * the rest stay queued. */
+cph_status cph_get_dbo_events(cph_ctx *ctx, cph_dbo_event *ev, int64_t cap, int64_t *n);
+/* Current block accumulators of one replica: well [C*5] = (steps, steps near 0,
+ * sum of lambda near 0, steps near 1, sum of lambda near 1); barrier [C*4] =
+ * (frames A, in-transition A, frames B, in-transition B) with A = all frames for
+ * lambda_p coordinates / protonated frames for tautomer coordinates, B =
+ * deprotonated frames.  Either pointer may be NULL. */
+cph_status cph_get_dbo_stats(cph_ctx *ctx, int32_t replica, double *well, double *barrier);
+
 /* Force on every atom [3N] (kJ mol^-1 nm^-1) and the full electrostatic potential
  * phi_i = (1/f) dE_coul/dq_i [N] (e/nm; real + exclusion + reciprocal + self +
  * net-charge terms), original order.  Either pointer may be NULL. */

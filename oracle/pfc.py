@@ -92,8 +92,8 @@ def quadrant_free_energies(h, d1p, d1t, pKa3, pH, T, kw, dbo=None):
         dbo = B.default_dbo(h, 2)
     beta = 1.0 / kT(T)
     (a0p, a1p, hp, _), (a0t, a1t, htp, htd) = dbo
-    xp, wp = _gl_nodes(_breaks((a0p, a1p)))
-    xt, wt = _gl_nodes(_breaks((a0t, a1t)))
+    xp, wp = _gl_nodes(_breaks((a0p, a1p)), sub=4)
+    xt, wt = _gl_nodes(_breaks((a0t, a1t)), sub=4)
     vp = vdw(xp, hp, 0.0, d1p, kw, a0p, a1p)[0]
     ht = B.tautomer_barrier(xp, htp, htd)[0]
     LP, LT = np.meshgrid(xp, xt, indexing="ij")
@@ -117,7 +117,8 @@ def pfc_3state(h, pKa3, pH, T, kw, dbo=None):
         a, b = quadrant_free_energies(h, v[0], v[1], pKa3, pH, T, kw, dbo)
         return [a - gd, b - ge]
     sol = optimize.root(res, [0.0, 0.0], method="hybr", tol=1e-14)
-    if sol.success and np.max(np.abs(res(sol.x))) < 1e-9 and np.all(np.abs(sol.x) <= D1_BOUND):
+    # hybr may report "not making good progress" once at the rounding floor: judge the residual
+    if np.max(np.abs(res(sol.x))) < 1e-9 and np.all(np.abs(sol.x) <= D1_BOUND):
         return float(sol.x[0]), float(sol.x[1])
     # unreachable targets (R22): nested saturating bisection - the tautomer split
     # G_eps - G_delta = dG_eps - dG_delta for d1_t inside, the macro deprotonation free

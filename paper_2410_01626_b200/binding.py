@@ -18,7 +18,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcph.so")
 
-CPH_ABI_VERSION = 1
+CPH_ABI_VERSION = 2
 STATUS = {0: "CPH_OK", 1: "CPH_E_INVALID", 2: "CPH_E_CUDA", 3: "CPH_E_DIVERGED", 4: "CPH_E_STATE",
           5: "CPH_E_OOM", 6: "CPH_E_UNSUPPORTED"}
 ENERGY_TERMS = ("LJ", "real", "excl", "self", "recip", "net", "bias", "KE_atoms", "KE_lambda", "total")
@@ -49,7 +49,21 @@ class cph_params(C.Structure):
                 ("barrier", C.c_double), ("wall_k", C.c_double), ("pH", _f64p), ("replica_seed", _u64p),
                 ("lambda0", _f64p), ("pos_replicas", _f32p), ("vel_replicas", _f32p),
                 ("frame_capacity", C.c_int32), ("cuda_stream", C.c_void_p), ("dev_alloc", ALLOC_FN),
-                ("dev_free", FREE_FN), ("alloc_ctx", C.c_void_p)]
+                ("dev_free", FREE_FN), ("alloc_ctx", C.c_void_p),
+                ("dbo_well", C.c_int32), ("dbo_barrier", C.c_int32), ("dbo_well_steps", C.c_int64),
+                ("dbo_barrier_steps", C.c_int64), ("dbo_censor_steps", C.c_int64), ("dbo_well_near", C.c_double),
+                ("dbo_residency", C.c_double), ("dbo_well_tol", C.c_double), ("dbo_well_gain", C.c_double),
+                ("dbo_well_cap", C.c_double), ("dbo_trans_lo", C.c_double), ("dbo_trans_hi", C.c_double),
+                ("dbo_target", C.c_double), ("dbo_target_tol", C.c_double), ("dbo_barrier_step", C.c_double),
+                ("dbo_barrier_min", C.c_double), ("dbo_barrier_max", C.c_double)]
+
+
+class cph_dbo_event(C.Structure):
+    _fields_ = [("step", C.c_int64), ("replica", C.c_int32), ("coord", C.c_int32), ("kind", C.c_int32),
+                ("pad", C.c_int32), ("old_value", C.c_double), ("new_value", C.c_double)]
+
+
+DBO_KINDS = ("well0", "well1", "barrier", "barrier_t_prot", "barrier_t_deprot")
 
 
 EXPORTS = {
@@ -68,6 +82,11 @@ EXPORTS = {
     "cph_get_energies": (C.c_int, [C.c_void_p, C.c_int32, _f64p]),
     "cph_get_bias_params": (C.c_int, [C.c_void_p, C.c_int32, _f64p]),
     "cph_get_frames": (C.c_int, [C.c_void_p, C.c_int32, _f32p, C.c_int64, _i64p, _i64p]),
+    "cph_get_frames_ex": (C.c_int, [C.c_void_p, C.c_int32, _f32p, _p(C.c_uint8), _i64p, C.c_int64, _i64p, _i64p]),
+    "cph_get_dbo_params": (C.c_int, [C.c_void_p, C.c_int32, _f64p]),
+    "cph_set_dbo_params": (C.c_int, [C.c_void_p, C.c_int32, _f64p]),
+    "cph_get_dbo_events": (C.c_int, [C.c_void_p, _p(cph_dbo_event), C.c_int64, _i64p]),
+    "cph_get_dbo_stats": (C.c_int, [C.c_void_p, C.c_int32, _f64p, _f64p]),
     "cph_get_forces": (C.c_int, [C.c_void_p, C.c_int32, _f32p, _f32p]),
     "cph_get_positions": (C.c_int, [C.c_void_p, C.c_int32, _f32p, _f32p]),
     "cph_get_pairlist": (C.c_int, [C.c_void_p, C.c_int32, _i32p, C.c_int64, _i64p]),
@@ -189,9 +208,15 @@ def cph_create(system, pH, replica_seed, *, lambda0=None, pos_replicas=None, vel
               "barrier", "wall_k"):
         if k in params:
             setattr(p, k, float(params[k]))
-    for k in ("pme_order", "nstlist", "nstout", "nstenergy", "frame_capacity"):
+    for k in ("pme_order", "nstlist", "nstout", "nstenergy", "frame_capacity", "dbo_well", "dbo_barrier",
+              "dbo_well_steps", "dbo_barrier_steps", "dbo_censor_steps"):
         if k in params:
             setattr(p, k, int(params[k]))
+    for k in ("dbo_well_near", "dbo_residency", "dbo_well_tol", "dbo_well_gain", "dbo_well_cap", "dbo_trans_lo",
+              "dbo_trans_hi", "dbo_target", "dbo_target_tol", "dbo_barrier_step", "dbo_barrier_min",
+              "dbo_barrier_max"):
+        if k in params:
+            setattr(p, k, float(params[k]))
     grid = overrides.get("pme_grid", getattr(system, "pme_grid", None))
     if grid is not None:
         p.pme_grid[:] = [int(g) for g in grid]
@@ -283,6 +308,46 @@ class Context:
         n, dropped = C.c_int64(), C.c_int64()
         _check(lib().cph_get_frames(self.h, r, _ptr(buf, C.c_float), cap, C.byref(n), C.byref(dropped)), self.h)
         return buf[: n.value * self.C].reshape(n.value, self.C), dropped.value
+
+    def cph_get_frames_ex(self, r, cap=1 << 20):
+        """(frames [n, C], censored [n, C] bool, steps [n], n_dropped)."""
+        cap = int(cap)
+        buf = np.zeros(max(cap, 1) * max(self.C, 1), np.float32)
+        cen = np.zeros(max(cap, 1) * max(self.C, 1), np.uint8)
+        st = np.zeros(max(cap, 1), np.int64)
+        n, dropped = C.c_int64(), C.c_int64()
+        _check(lib().cph_get_frames_ex(self.h, r, _ptr(buf, C.c_float), _ptr(cen, C.c_uint8), _ptr(st, C.c_int64),
+                                       cap, C.byref(n), C.byref(dropped)), self.h)
+        k = n.value
+        return (buf[: k * self.C].reshape(k, self.C), cen[: k * self.C].reshape(k, self.C).astype(bool),
+                st[:k].copy(), dropped.value)
+
+    def cph_get_dbo_params(self, r):
+        """[C, 4]: (a0, a1, h_prot, h_deprot) per coordinate."""
+        p = np.zeros(4 * self.C)
+        _check(lib().cph_get_dbo_params(self.h, r, _ptr(p, C.c_double)), self.h)
+        return p.reshape(self.C, 4)
+
+    def cph_set_dbo_params(self, r, params):
+        p = np.ascontiguousarray(params, np.float64).reshape(-1)
+        _check(lib().cph_set_dbo_params(self.h, r, _ptr(p, C.c_double)), self.h)
+
+    def cph_get_dbo_events(self, cap=4096):
+        """Drained adjustment log: list of (step, replica, coord, kind name, old, new)."""
+        out = []
+        buf = (cph_dbo_event * cap)()
+        n = C.c_int64()
+        while True:
+            _check(lib().cph_get_dbo_events(self.h, buf, cap, C.byref(n)), self.h)
+            out += [(e.step, e.replica, e.coord, DBO_KINDS[e.kind], e.old_value, e.new_value) for e in buf[: n.value]]
+            if n.value < cap:
+                return out
+
+    def cph_get_dbo_stats(self, r):
+        w = np.zeros(5 * self.C)
+        b = np.zeros(4 * self.C)
+        _check(lib().cph_get_dbo_stats(self.h, r, _ptr(w, C.c_double), _ptr(b, C.c_double)), self.h)
+        return w.reshape(self.C, 5), b.reshape(self.C, 4)
 
     def cph_get_forces(self, r):
         f = np.zeros((self.N, 3), np.float32)

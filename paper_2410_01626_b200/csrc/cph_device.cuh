@@ -81,21 +81,36 @@ __device__ __forceinline__ float min_image_rn(float dx, float L, float invL) {
 //   Vdw: cubic Hermite through (0,0,0), (0.5,h,0), (1,d1,0), mirrored outside
 //   [0,1], quartic walls k_w (l+0.1)^4 below -0.1 and k_w (l-1.1)^4 above 1.1.
 // ---------------------------------------------------------------------------------
-__host__ __device__ inline void vdw_eval(double lam, double h, double d1, double kw, double *v,
-                                         double *dv) {
+// Double well with DBO-movable well centres a0, a1:
+// cubic Hermite knots (a0, 0), (m, h), (a1, d1), m = (a0 + a1)/2, zero slopes; mirrored about
+// a0 / a1 outside [a0, a1]; quartic walls k_w (lam + 0.1)^4 below -0.1 and k_w (lam - 1.1)^4
+// above 1.1 (R5, R23).  Returns V, dV/dlam and dV/dh (V is linear in h).
+__host__ __device__ inline void vdw_eval(double lam, double a0, double a1, double h, double d1, double kw,
+                                         double *v, double *dv, double *dh) {
+  const double m = 0.5 * (a0 + a1);
   double x = lam, sgn = 1.0;
-  if (lam < 0.0) { x = -lam; sgn = -1.0; }
-  else if (lam > 1.0) { x = 2.0 - lam; sgn = -1.0; }
-  x = x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x);
-  double a, b, t;
-  if (x <= 0.5) { a = 0.0; b = h; t = 2.0 * x; }
-  else { a = h; b = d1; t = 2.0 * (x - 0.5); }
-  double val = a + (b - a) * t * t * (3.0 - 2.0 * t);
-  double der = sgn * 2.0 * (b - a) * 6.0 * t * (1.0 - t);
-  if (lam < -0.1) { double w = lam + 0.1; val += kw * w * w * w * w; der += 4.0 * kw * w * w * w; }
-  else if (lam > 1.1) { double w = lam - 1.1; val += kw * w * w * w * w; der += 4.0 * kw * w * w * w; }
+  if (lam < a0) { x = 2.0 * a0 - lam; sgn = -1.0; }
+  else if (lam > a1) { x = 2.0 * a1 - lam; sgn = -1.0; }
+  x = x < a0 ? a0 : (x > a1 ? a1 : x);
+  double a, b, t, w;
+  bool left = x <= m;
+  if (left) { a = 0.0; b = h; w = m - a0; t = (x - a0) / w; }
+  else { a = h; b = d1; w = a1 - m; t = (x - m) / w; }
+  const double s = t * t * (3.0 - 2.0 * t);
+  double val = a + (b - a) * s;
+  double der = sgn * (b - a) * 6.0 * t * (1.0 - t) / w;
+  if (lam < -0.1) { double q = lam + 0.1; val += kw * q * q * q * q; der += 4.0 * kw * q * q * q; }
+  else if (lam > 1.1) { double q = lam - 1.1; val += kw * q * q * q * q; der += 4.0 * kw * q * q * q; }
   *v = val;
   *dv = der;
+  if (dh) *dh = left ? s : 1.0 - s;
+}
+
+// barrier of a tautomer coordinate keyed by protonation, smooth in lambda_p (R25)
+__host__ __device__ inline void tautomer_barrier(double lp, double hp, double hd, double *h, double *dh) {
+  const double x = lp < 0.0 ? 0.0 : (lp > 1.0 ? 1.0 : lp);
+  *h = hp + (hd - hp) * x * x * (3.0 - 2.0 * x);
+  *dh = (lp > 0.0 && lp < 1.0) ? (hd - hp) * 6.0 * x * (1.0 - x) : 0.0;
 }
 
 __host__ __device__ inline void vmm_eval(const double *c, double lp, double lt, double *v, double *dp,

@@ -65,6 +65,9 @@ struct KParams {
   double Q_fixed, Q2_fixed;    // sum and sum of squares of fixed charges (per replica identical)
   double h_barrier, wall_k;
   int fcap;                    // frame capacity
+  // DBO statistics: on/off and the proximity / transition bands
+  int dbo_on;
+  double dbo_near, dbo_trans_lo, dbo_trans_hi;
 };
 
 struct DevBufs {
@@ -103,6 +106,23 @@ struct DevBufs {
   uint64_t *seed = nullptr;                         // [R]
   double *phi_lam = nullptr;                        // [R*nlam] total phi of lambda atoms
   int *k_group = nullptr;                           // [nlam] group of each lambda atom
+  // DBO
+  double *dw = nullptr;                             // [R*C*4] a0, a1, h_prot, h_deprot
+  double *dbo_well = nullptr;                       // [R*C*5] block accumulators (well)
+  double *dbo_bar = nullptr;                        // [R*C*4] block accumulators (barrier)
+  int *c_group = nullptr;                           // [C] group of each coordinate
+  int *c_lp = nullptr;                              // [C] lambda_p coordinate of a tautomer coordinate, else -1
+  long long *cens = nullptr;                        // [R*G*2] censor window (from, until]
+  unsigned char *frame_cens = nullptr;              // [R*fcap*C]
+  long long *frame_step = nullptr;                  // [R*fcap]
+};
+
+struct DboConfig {
+  int well = 0, barrier = 0;
+  long long well_steps = 20000, barrier_steps = 500000, censor_steps = 5000;
+  double near = 0.2, residency = 0.7, tol = 0.03, gain = 0.5, cap = 0.08;
+  double trans_lo = 0.2, trans_hi = 0.8, target = 0.25, target_tol = 0.05;
+  double bstep = 1.0, bmin = 1.0, bmax = 20.0;
 };
 
 struct Ctx {
@@ -123,6 +143,12 @@ struct Ctx {
   std::vector<int> h_excl_ptr, h_excl_idx;
   std::vector<uint64_t> h_seed;
   std::vector<double> h_d1;                         // [R*C]
+  std::vector<double> h_dG;                         // [R*G*3]
+  std::vector<double> h_dw;                         // [R*C*4] DBO parameters (host master copy)
+  std::vector<int> h_c_group, h_c_lp;               // [C]
+  std::vector<long long> h_cens;                    // [R*G*2]
+  std::vector<cph_dbo_event> events;                // undrained DBO log
+  DboConfig dbo;
   int *h_flags_mapped = nullptr;                    // host view of a mapped flag copy
   int *d_flags_mapped = nullptr;
   long long host_step = 0;
@@ -146,10 +172,10 @@ int launch_lambda_reduce(Ctx &c, cudaStream_t s, int mode);       // 0 init eval
 int launch_lambda_open(Ctx &c, cudaStream_t s);
 int launch_set_charges(Ctx &c, cudaStream_t s);
 
-// host PFC (pfc.cpp)
-bool pfc_two_state(double h, double pKa, double pH, double T, double kw, double *d1, std::string *err);
-bool pfc_three_state(double h, const double pKa3[3], double pH, double T, double kw, double *d1p,
-                     double *d1t, std::string *err);
+// host PFC (pfc.cu); dw = (a0, a1, h_prot, h_deprot) of each coordinate of the site
+bool pfc_two_state(const double dw[4], double pKa, double pH, double T, double kw, double *d1, std::string *err);
+bool pfc_three_state(const double dwp[4], const double dwt[4], const double pKa3[3], double pH, double T,
+                     double kw, double *d1p, double *d1t, std::string *err);
 double delta_g(double pKa, double pH, double T);
 
 }  // namespace cph

@@ -1,6 +1,10 @@
 // Host runtime behind include/cph.h: validation, device memory, PFC, cuFFT plans, step
 // scheduling (CUDA graph per nstlist block, nonbonded || PME on two streams), getters.
 #include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <thread>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -104,32 +108,58 @@ bool finite_arr(const double *p, size_t n) {
   return true;
 }
 
-cph_status run_pfc(Ctx &c, int r) {
+// PFC of replica r (all groups, or the groups flagged in `only`), with the current DBO
+// parameters of each coordinate: host arithmetic only, results in h_d1 / h_dG
+static bool compute_pfc(Ctx &c, int r, const std::vector<char> *only, std::string *err) {
   const KParams &kp = c.kp;
   const double pH = c.h_pH[r];
-  std::vector<double> dG((size_t)kp.G * 3), d1((size_t)kp.C);
+  double *dG = c.h_dG.data() + (size_t)r * kp.G * 3;
+  double *d1 = c.h_d1.data() + (size_t)r * kp.C;
+  const double *dw = c.h_dw.data() + (size_t)r * kp.C * 4;
   for (int g = 0; g < kp.G; ++g) {
     const double *pk = &c.h_pKa[(size_t)g * 3];
     for (int k = 0; k < 3; ++k) dG[(size_t)g * 3 + k] = delta_g(pk[k], pH, kp.kT / kBoltz);
+    if (only && !(*only)[g]) continue;
     const int c0 = c.h_cptr[g];
-    std::string err;
-    if (c.h_group_kind[g] == 2) {
-      if (!pfc_two_state(kp.h_barrier, pk[0], pH, kp.kT / kBoltz, kp.wall_k, &d1[c0], &err)) {
-        c.err = err;
-        return CPH_E_INVALID;
-      }
-    } else {
-      if (!pfc_three_state(kp.h_barrier, pk, pH, kp.kT / kBoltz, kp.wall_k, &d1[c0], &d1[c0 + 1], &err)) {
-        c.err = err;
-        return CPH_E_INVALID;
+    const bool ok = c.h_group_kind[g] == 2
+                        ? pfc_two_state(dw + 4 * c0, pk[0], pH, kp.kT / kBoltz, kp.wall_k, &d1[c0], err)
+                        : pfc_three_state(dw + 4 * c0, dw + 4 * (c0 + 1), pk, pH, kp.kT / kBoltz, kp.wall_k, &d1[c0],
+                                          &d1[c0 + 1], err);
+    if (!ok) return false;
+  }
+  return true;
+}
+
+// PFC for a set of replicas (host threads, one replica per task), then one upload
+cph_status run_pfc_many(Ctx &c, const std::vector<int> &reps, const std::vector<std::vector<char>> *only = nullptr) {
+  if (reps.empty()) return CPH_OK;
+  const int nt = (int)std::max<size_t>(1, std::min<size_t>(reps.size(), std::thread::hardware_concurrency()));
+  std::atomic<size_t> next{0};
+  std::atomic<bool> failed{false};
+  std::string ferr;
+  std::mutex mu;
+  auto work = [&]() {
+    for (size_t k; (k = next.fetch_add(1)) < reps.size();) {
+      std::string e;
+      if (!compute_pfc(c, reps[k], only ? &(*only)[reps[k]] : nullptr, &e)) {
+        std::lock_guard<std::mutex> lk(mu);
+        failed = true;
+        ferr = e;
       }
     }
-  }
-  std::copy(d1.begin(), d1.end(), c.h_d1.begin() + (size_t)r * kp.C);
-  if (kp.C) CK(cudaMemcpy(c.d.d1 + (size_t)r * kp.C, d1.data(), sizeof(double) * kp.C, cudaMemcpyHostToDevice));
-  if (kp.G) CK(cudaMemcpy(c.d.g_dG + (size_t)r * kp.G * 3, dG.data(), sizeof(double) * kp.G * 3, cudaMemcpyHostToDevice));
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(work);
+  work();
+  for (auto &t : th) t.join();
+  if (failed) { c.err = ferr; return CPH_E_INVALID; }
+  const KParams &kp = c.kp;
+  if (kp.C) CK(cudaMemcpy(c.d.d1, c.h_d1.data(), sizeof(double) * c.h_d1.size(), cudaMemcpyHostToDevice));
+  if (kp.G) CK(cudaMemcpy(c.d.g_dG, c.h_dG.data(), sizeof(double) * c.h_dG.size(), cudaMemcpyHostToDevice));
   return CPH_OK;
 }
+
+cph_status run_pfc(Ctx &c, int r) { return run_pfc_many(c, std::vector<int>{r}); }
 
 __global__ void k_set_end(long long *end, long long v) { *end = v; }
 
@@ -249,6 +279,23 @@ void cph_default_params(cph_params *p) {
   p->barrier = 6.0;
   p->wall_k = 1e6;
   p->frame_capacity = 1024;
+  p->dbo_well = 0;
+  p->dbo_barrier = 0;
+  p->dbo_well_steps = 20000;       // 40 ps
+  p->dbo_barrier_steps = 500000;   // 1 ns
+  p->dbo_censor_steps = 5000;      // 10 ps
+  p->dbo_well_near = 0.2;
+  p->dbo_residency = 0.7;
+  p->dbo_well_tol = 0.03;
+  p->dbo_well_gain = 0.5;
+  p->dbo_well_cap = 0.08;
+  p->dbo_trans_lo = 0.2;
+  p->dbo_trans_hi = 0.8;
+  p->dbo_target = 0.25;
+  p->dbo_target_tol = 0.05;
+  p->dbo_barrier_step = 1.0;
+  p->dbo_barrier_min = 1.0;
+  p->dbo_barrier_max = 20.0;
 }
 
 const char *cph_last_error(const cph_ctx *ctx) { return ctx ? ctx->c.err.c_str() : g_create_err.c_str(); }
@@ -293,6 +340,18 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   if (prm->nstlist < 1 || prm->nstout < 1 || prm->nstenergy < 1 || prm->frame_capacity < 1)
     return bad("nstlist, nstout, nstenergy, frame_capacity must be >= 1");
   if (prm->mode != 0 && prm->mode != 1) return bad("mode must be 0 or 1");
+  if (prm->dbo_well || prm->dbo_barrier) {
+    if ((prm->dbo_well && (prm->dbo_well_steps < 1 || prm->dbo_well_steps % prm->nstlist)) ||
+        (prm->dbo_barrier && (prm->dbo_barrier_steps < 1 || prm->dbo_barrier_steps % prm->nstlist)) ||
+        prm->dbo_censor_steps < 0)
+      return bad("DBO block lengths must be positive multiples of nstlist, censor window >= 0");
+    if (!(prm->dbo_well_near > 0.0 && prm->dbo_well_near < 0.5) || !(prm->dbo_residency >= 0.0) ||
+        !(prm->dbo_well_tol >= 0.0) || !(prm->dbo_well_gain >= 0.0) ||
+        !(prm->dbo_well_cap >= 0.0 && prm->dbo_well_cap <= 0.2) ||
+        !(prm->dbo_trans_lo < prm->dbo_trans_hi) || !(prm->dbo_barrier_step >= 0.0) ||
+        !(prm->dbo_barrier_min > 0.0 && prm->dbo_barrier_min <= prm->dbo_barrier_max && prm->dbo_barrier_max <= 100.0))
+      return bad("invalid DBO rule constant");
+  }
   if (!prm->pH || !prm->replica_seed) return bad("pH and replica_seed arrays are required");
   if (!finite_arr(prm->pH, R)) return bad("non-finite pH");
   if (prm->pme_order != 4) { c.err = "only pme_order 4 is implemented"; return fail_create(ctx, CPH_E_UNSUPPORTED); }
@@ -423,6 +482,21 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   kp.h_barrier = prm->barrier;
   kp.wall_k = prm->wall_k;
   kp.fcap = prm->frame_capacity;
+  {
+    DboConfig &b = c.dbo;
+    const bool on = prm->mode == 0 && (prm->dbo_well || prm->dbo_barrier);
+    b.well = on && prm->dbo_well;
+    b.barrier = on && prm->dbo_barrier;
+    b.well_steps = prm->dbo_well_steps; b.barrier_steps = prm->dbo_barrier_steps;
+    b.censor_steps = prm->dbo_censor_steps;
+    b.near = prm->dbo_well_near; b.residency = prm->dbo_residency; b.tol = prm->dbo_well_tol;
+    b.gain = prm->dbo_well_gain; b.cap = prm->dbo_well_cap;
+    b.trans_lo = prm->dbo_trans_lo; b.trans_hi = prm->dbo_trans_hi;
+    b.target = prm->dbo_target; b.target_tol = prm->dbo_target_tol;
+    b.bstep = prm->dbo_barrier_step; b.bmin = prm->dbo_barrier_min; b.bmax = prm->dbo_barrier_max;
+    kp.dbo_on = on ? 1 : 0;
+    kp.dbo_near = b.near; kp.dbo_trans_lo = b.trans_lo; kp.dbo_trans_hi = b.trans_hi;
+  }
   kp.Q_fixed = 0.0; kp.Q2_fixed = 0.0;
   for (int i = 0; i < N; ++i)
     if (lslot[i] < 0) { kp.Q_fixed += sys->charge[i]; kp.Q2_fixed += (double)sys->charge[i] * sys->charge[i]; }
@@ -488,6 +562,14 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   d.done_counter = dalloc<int>(c, 1);
   d.flags = dalloc<int>(c, FLAG_COUNT);
   d.seed = dalloc<uint64_t>(c, R);
+  d.dw = dalloc<double>(c, (size_t)R * C * 4);
+  d.dbo_well = dalloc<double>(c, (size_t)R * C * 5);
+  d.dbo_bar = dalloc<double>(c, (size_t)R * C * 4);
+  d.c_group = dalloc<int>(c, C);
+  d.c_lp = dalloc<int>(c, C);
+  d.cens = dalloc<long long>(c, (size_t)R * G * 2);
+  d.frame_cens = dalloc<unsigned char>(c, (size_t)R * kp.fcap * C);
+  d.frame_step = dalloc<long long>(c, (size_t)R * kp.fcap);
   for (void *p : {(void *)d.xyzq, (void *)d.nbl, (void *)d.grid, (void *)d.cgrid, (void *)d.flags, (void *)d.seed})
     if (!p) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
   if (c.allocations.size() < 40) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
@@ -522,6 +604,19 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   c.h_seed.assign(prm->replica_seed, prm->replica_seed + R);
   c.h_pH.assign(prm->pH, prm->pH + R);
   c.h_d1.assign((size_t)R * C, 0.0);
+  c.h_dG.assign((size_t)R * G * 3, 0.0);
+  c.h_dw.resize((size_t)R * C * 4);
+  for (size_t k = 0; k < (size_t)R * C; ++k) {
+    c.h_dw[4 * k] = 0.0; c.h_dw[4 * k + 1] = 1.0;
+    c.h_dw[4 * k + 2] = c.h_dw[4 * k + 3] = prm->barrier;
+  }
+  c.h_c_group.assign(C, 0);
+  c.h_c_lp.assign(C, -1);
+  for (int g = 0; g < G; ++g) {
+    for (int k = c.h_cptr[g]; k < c.h_cptr[g + 1]; ++k) c.h_c_group[k] = g;
+    if (c.h_group_kind[g] == 3) c.h_c_lp[c.h_cptr[g] + 1] = c.h_cptr[g];
+  }
+  c.h_cens.assign((size_t)R * G * 2, 0);
 
 #define UP(dst, src, n) CK(cudaMemcpy(dst, src, sizeof(*(src)) * (n), cudaMemcpyHostToDevice))
   {
@@ -541,7 +636,12 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
           for (int k = c.h_group_ptr[g]; k < c.h_group_ptr[g + 1]; ++k) kg[k] = g;
         UP(d.k_group, kg.data(), nlam);
       }
-      if (C) UP(d.lam, lam0.data(), (size_t)R * C);
+      if (C) {
+        UP(d.lam, lam0.data(), (size_t)R * C);
+        UP(d.dw, c.h_dw.data(), c.h_dw.size());
+        UP(d.c_group, c.h_c_group.data(), C);
+        UP(d.c_lp, c.h_c_lp.data(), C);
+      }
       UP(d.seed, c.h_seed.data(), R);
       return CPH_OK;
     };
@@ -549,8 +649,10 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     if (st != CPH_OK) return fail_create(ctx, st);
   }
 #undef UP
-  for (int r = 0; r < R; ++r) {
-    cph_status st = run_pfc(c, r);
+  {
+    std::vector<int> all(R);
+    for (int r = 0; r < R; ++r) all[r] = r;
+    cph_status st = run_pfc_many(c, all);
     if (st != CPH_OK) return fail_create(ctx, st);
   }
   // cuFFT plans (batched over replicas)
@@ -612,13 +714,8 @@ cph_status cph_set_pH(cph_ctx *ctx, int32_t replica, double pH) {
   return st;
 }
 
-cph_status cph_step(cph_ctx *ctx, int64_t n_steps) {
-  if (!ctx) return CPH_E_INVALID;
-  Ctx &c = ctx->c;
-  if (n_steps < 0) { c.err = "n_steps < 0"; return CPH_E_INVALID; }
-  if (n_steps == 0) return CPH_OK;
-  cudaSetDevice(c.device);
-  const long long end = c.host_step + n_steps;
+// steps host_step -> end as one asynchronous segment (graphs of nstlist steps where aligned)
+static cph_status run_segment(Ctx &c, long long end) {
   k_set_end<<<1, 1, 0, c.stream>>>(c.d.end_step, end);
   int k = 1;
   k += launch_lambda_open(c, c.stream);
@@ -639,6 +736,116 @@ cph_status cph_step(cph_ctx *ctx, int64_t n_steps) {
   k += launch_close(c, c.stream, 1);
   c.launches += k;
   CK(cudaGetLastError());
+  return CPH_OK;
+}
+
+// ---- DBO controllers (R23-R26) -----------------------------
+static double well_decide(const DboConfig &b, double shift, double n, double n_near, double sum_near, double ideal) {
+  if (n <= 0.0 || n_near <= 0.0 || !(n_near / n > b.residency)) return shift;
+  const double diff = ideal - sum_near / n_near;
+  if (!(std::fabs(diff) > b.tol)) return shift;
+  return std::min(b.cap, std::max(-b.cap, shift + b.gain * diff));
+}
+
+static double barrier_decide(const DboConfig &b, double h, double n, double n_trans) {
+  if (n <= 0.0) return h;
+  const double frac = n_trans / n;
+  if (frac < b.target - b.target_tol) return std::max(b.bmin, h - b.bstep);
+  if (frac > b.target + b.target_tol) return std::min(b.bmax, h + b.bstep);
+  return h;
+}
+
+// End of step S = host_step: run the due block rules for every replica, log and censor the
+// adjusted sites, refresh their PFC and re-evaluate the forces at the unchanged state so
+// step S+1 starts on the new bias.
+static cph_status dbo_block_end(Ctx &c) {
+  const KParams &kp = c.kp;
+  const DboConfig &b = c.dbo;
+  const long long S = c.host_step;
+  const bool do_well = b.well && S % b.well_steps == 0;
+  const bool do_bar = b.barrier && S % b.barrier_steps == 0;
+  if (!do_well && !do_bar) return CPH_OK;
+  const int R = kp.R, C = kp.C, G = kp.G;
+  std::vector<double> wst((size_t)R * C * 5), bst((size_t)R * C * 4);
+  CK(cudaStreamSynchronize(c.stream));
+  if (do_well) {
+    CK(cudaMemcpy(wst.data(), c.d.dbo_well, sizeof(double) * wst.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(c.d.dbo_well, 0, sizeof(double) * wst.size()));
+  }
+  if (do_bar) {
+    CK(cudaMemcpy(bst.data(), c.d.dbo_bar, sizeof(double) * bst.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(c.d.dbo_bar, 0, sizeof(double) * bst.size()));
+  }
+  std::vector<std::vector<char>> changed_all(R, std::vector<char>(G, 0));
+  std::vector<int> reps;
+  for (int r = 0; r < R; ++r) {
+    std::vector<char> &changed = changed_all[r];
+    auto log = [&](int k, int kind, double o, double n) {
+      c.events.push_back(cph_dbo_event{S, r, k, kind, 0, o, n});
+      changed[c.h_c_group[k]] = 1;
+    };
+    double *dw = c.h_dw.data() + (size_t)r * C * 4;
+    if (do_well)
+      for (int k = 0; k < C; ++k) {
+        const double *a = wst.data() + ((size_t)r * C + k) * 5;
+        double *w = dw + 4 * k;
+        const double a0 = well_decide(b, w[0], a[0], a[1], a[2], 0.0);
+        const double a1 = 1.0 + well_decide(b, w[1] - 1.0, a[0], a[3], a[4], 1.0);
+        if (a0 != w[0]) { log(k, CPH_DBO_WELL0, w[0], a0); w[0] = a0; }
+        if (a1 != w[1]) { log(k, CPH_DBO_WELL1, w[1], a1); w[1] = a1; }
+      }
+    if (do_bar)
+      for (int k = 0; k < C; ++k) {
+        const double *a = bst.data() + ((size_t)r * C + k) * 4;
+        double *w = dw + 4 * k;
+        if (c.h_c_lp[k] < 0) {
+          const double h = barrier_decide(b, w[2], a[0], a[1]);
+          if (h != w[2]) { log(k, CPH_DBO_BARRIER, w[2], h); w[2] = w[3] = h; }
+        } else {
+          const double hp = barrier_decide(b, w[2], a[0], a[1]);
+          const double hd = barrier_decide(b, w[3], a[2], a[3]);
+          if (hp != w[2]) { log(k, CPH_DBO_BARRIER_T_PROT, w[2], hp); w[2] = hp; }
+          if (hd != w[3]) { log(k, CPH_DBO_BARRIER_T_DEPROT, w[3], hd); w[3] = hd; }
+        }
+      }
+    bool rc = false;
+    for (int g = 0; g < G; ++g)
+      if (changed[g]) {
+        rc = true;
+        long long *w = c.h_cens.data() + ((size_t)r * G + g) * 2;   // (from, until]
+        if (!(S < w[1])) w[0] = S;
+        w[1] = S + b.censor_steps;
+      }
+    if (rc) reps.push_back(r);
+  }
+  if (reps.empty()) return CPH_OK;
+  if (cph_status st = run_pfc_many(c, reps, &changed_all)) return st;
+  CK(cudaMemcpy(c.d.dw, c.h_dw.data(), sizeof(double) * c.h_dw.size(), cudaMemcpyHostToDevice));
+  if (G) CK(cudaMemcpy(c.d.cens, c.h_cens.data(), sizeof(long long) * c.h_cens.size(), cudaMemcpyHostToDevice));
+  return evaluate_here(c);
+}
+
+static long long next_dbo_boundary(const Ctx &c) {
+  long long nb = LLONG_MAX;
+  const long long s = c.host_step;
+  if (c.dbo.well) nb = std::min(nb, (s / c.dbo.well_steps + 1) * c.dbo.well_steps);
+  if (c.dbo.barrier) nb = std::min(nb, (s / c.dbo.barrier_steps + 1) * c.dbo.barrier_steps);
+  return nb;
+}
+
+cph_status cph_step(cph_ctx *ctx, int64_t n_steps) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  if (n_steps < 0) { c.err = "n_steps < 0"; return CPH_E_INVALID; }
+  if (n_steps == 0) return CPH_OK;
+  cudaSetDevice(c.device);
+  const long long end = c.host_step + n_steps;
+  while (c.host_step < end) {
+    const long long seg = c.kp.dbo_on ? std::min(end, next_dbo_boundary(c)) : end;
+    cph_status st = run_segment(c, seg);
+    if (st) return st;
+    if (c.kp.dbo_on && (st = dbo_block_end(c))) return st;
+  }
   return CPH_OK;
 }
 
@@ -692,28 +899,98 @@ cph_status cph_get_energies(cph_ctx *ctx, int32_t r, double *e) {
   return CPH_OK;
 }
 
-cph_status cph_get_frames(cph_ctx *ctx, int32_t r, float *buf, int64_t cap, int64_t *n_frames, int64_t *n_dropped) {
+cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t r, float *buf, uint8_t *censored, int64_t *steps, int64_t cap,
+                             int64_t *n_frames, int64_t *n_dropped) {
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
   if (st || (st = cph_sync(ctx))) return st;
+  if (cap < 0) { c.err = "cap < 0"; return CPH_E_INVALID; }
   const KParams &kp = c.kp;
   long long total = 0;
   CK(cudaMemcpy(&total, c.d.frame_total + r, sizeof(long long), cudaMemcpyDeviceToHost));
   const long long avail = std::min<long long>(total, kp.fcap);
   const long long take = std::min<long long>(avail, cap);
   std::vector<float> all((size_t)kp.fcap * kp.C);
-  if (kp.C) CK(cudaMemcpy(all.data(), c.d.frames + (size_t)r * kp.fcap * kp.C, sizeof(float) * all.size(), cudaMemcpyDeviceToHost));
+  std::vector<unsigned char> cens((size_t)kp.fcap * kp.C);
+  std::vector<long long> fst(kp.fcap);
+  if (kp.C) {
+    CK(cudaMemcpy(all.data(), c.d.frames + (size_t)r * kp.fcap * kp.C, sizeof(float) * all.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cens.data(), c.d.frame_cens + (size_t)r * kp.fcap * kp.C, cens.size(), cudaMemcpyDeviceToHost));
+  }
+  CK(cudaMemcpy(fst.data(), c.d.frame_step + (size_t)r * kp.fcap, sizeof(long long) * kp.fcap, cudaMemcpyDeviceToHost));
   // oldest retained frame index = total - avail; we return the newest `take` frames in order
   const long long first = total - take;
-  for (long long f = 0; f < take && buf; ++f) {
+  for (long long f = 0; f < take; ++f) {
     const long long slot = (first + f) % kp.fcap;
-    for (int k = 0; k < kp.C; ++k) buf[f * kp.C + k] = all[(size_t)slot * kp.C + k];
+    for (int k = 0; k < kp.C; ++k) {
+      if (buf) buf[f * kp.C + k] = all[(size_t)slot * kp.C + k];
+      if (censored) censored[f * kp.C + k] = cens[(size_t)slot * kp.C + k];
+    }
+    if (steps) steps[f] = fst[slot];
   }
   if (n_frames) *n_frames = take;
   if (n_dropped) *n_dropped = total - take;
   const long long zero = 0;
   CK(cudaMemcpy(c.d.frame_total + r, &zero, sizeof(long long), cudaMemcpyHostToDevice));
+  return CPH_OK;
+}
+
+cph_status cph_get_frames(cph_ctx *ctx, int32_t r, float *buf, int64_t cap, int64_t *n_frames, int64_t *n_dropped) {
+  return cph_get_frames_ex(ctx, r, buf, nullptr, nullptr, cap, n_frames, n_dropped);
+}
+
+cph_status cph_get_dbo_params(cph_ctx *ctx, int32_t r, double *p) {
+  if (!ctx || !p) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st) return st;
+  std::copy(c.h_dw.begin() + (size_t)r * c.kp.C * 4, c.h_dw.begin() + (size_t)(r + 1) * c.kp.C * 4, p);
+  return CPH_OK;
+}
+
+cph_status cph_set_dbo_params(cph_ctx *ctx, int32_t r, const double *p) {
+  if (!ctx || !p) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st) return st;
+  const int C = c.kp.C;
+  if (!finite_arr(p, (size_t)C * 4)) { c.err = "non-finite DBO parameter"; return CPH_E_INVALID; }
+  for (int k = 0; k < C; ++k) {
+    const double *w = p + 4 * k;
+    if (std::fabs(w[0]) > 0.2 || std::fabs(w[1] - 1.0) > 0.2 || !(w[2] > 0.0 && w[2] <= 100.0) ||
+        !(w[3] > 0.0 && w[3] <= 100.0) || (c.h_c_lp[k] < 0 && w[2] != w[3])) {
+      c.err = "DBO parameters out of range (|a0| <= 0.2, |a1-1| <= 0.2, 0 < h <= 100, lambda_p: h_prot == h_deprot)";
+      return CPH_E_INVALID;
+    }
+  }
+  cudaSetDevice(c.device);
+  CK(cudaStreamSynchronize(c.stream));
+  std::copy(p, p + (size_t)C * 4, c.h_dw.begin() + (size_t)r * C * 4);
+  if (C) CK(cudaMemcpy(c.d.dw + (size_t)r * C * 4, p, sizeof(double) * C * 4, cudaMemcpyHostToDevice));
+  if ((st = run_pfc(c, r))) return st;
+  if ((st = evaluate_here(c))) return st;
+  return check_flags(c);
+}
+
+cph_status cph_get_dbo_events(cph_ctx *ctx, cph_dbo_event *ev, int64_t cap, int64_t *n) {
+  if (!ctx || cap < 0 || (cap > 0 && !ev)) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  const int64_t take = std::min<int64_t>(cap, (int64_t)c.events.size());
+  std::copy(c.events.begin(), c.events.begin() + take, ev);
+  c.events.erase(c.events.begin(), c.events.begin() + take);
+  if (n) *n = take;
+  return CPH_OK;
+}
+
+cph_status cph_get_dbo_stats(cph_ctx *ctx, int32_t r, double *well, double *barrier) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  const size_t C = c.kp.C;
+  if (well && C) CK(cudaMemcpy(well, c.d.dbo_well + r * C * 5, sizeof(double) * C * 5, cudaMemcpyDeviceToHost));
+  if (barrier && C) CK(cudaMemcpy(barrier, c.d.dbo_bar + r * C * 4, sizeof(double) * C * 4, cudaMemcpyDeviceToHost));
   return CPH_OK;
 }
 

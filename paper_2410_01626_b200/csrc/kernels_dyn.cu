@@ -189,18 +189,23 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
       vphp = (1.0 - lt) * dG[1] + lt * dG[2];
       vpht = lp * (dG[2] - dG[1]);
     }
+    // double wells with the DBO parameters (a0, a1, h_prot, h_deprot) of each coordinate
+    const double *wp = d.dw + ic * 4;
     double vd, vdp;
-    vdw_eval(lp, kp.h_barrier, d.d1[ic], kp.wall_k, &vd, &vdp);
+    vdw_eval(lp, wp[0], wp[1], wp[2], d.d1[ic], kp.wall_k, &vd, &vdp, nullptr);
     d.dvdl_coul[ic] = f * sp;
-    d.dvdl_bias[ic] = vmp + vphp + vdp;
     ebias += vm + vph + vd;
     if (kind == 3) {
-      double vd2, vdt;
-      vdw_eval(lt, kp.h_barrier, d.d1[ic + 1], kp.wall_k, &vd2, &vdt);
+      const double *wt = wp + 4;
+      double ht, dht, vd2, vdt, vdh;
+      tautomer_barrier(lp, wt[2], wt[3], &ht, &dht);
+      vdw_eval(lt, wt[0], wt[1], ht, d.d1[ic + 1], kp.wall_k, &vd2, &vdt, &vdh);
       d.dvdl_coul[ic + 1] = f * st;
       d.dvdl_bias[ic + 1] = vmt + vpht + vdt;
+      vdp += vdh * dht;
       ebias += vd2;
     }
+    d.dvdl_bias[ic] = vmp + vphp + vdp;
   }
   ebias = block_sum_d(ebias);   // includes __syncthreads: dV/dlambda visible to the block
   // closing half kick, frames, TI accumulation, divergence
@@ -218,13 +223,33 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
       d.lamv[ix] = v;
     }
     kel += 0.5 * kp.m_lam * v * v;
-    if (frame) d.frames[((size_t)r * kp.fcap + fslot) * kp.C + c] = (float)l;
+    if (frame) {
+      const size_t fi = ((size_t)r * kp.fcap + fslot) * kp.C + c;
+      d.frames[fi] = (float)l;
+      const long long *cw = d.cens + ((size_t)r * kp.G + d.c_group[c]) * 2;
+      d.frame_cens[fi] = (m > cw[0] && m <= cw[1]) ? 1 : 0;
+    }
+    if (kp.dbo_on && dyn && mode == 1) {
+      // DBO block statistics of the completed step m (R24)
+      double *aw = d.dbo_well + ix * 5;
+      aw[0] += 1.0;
+      if (l < kp.dbo_near) { aw[1] += 1.0; aw[2] += l; }
+      else if (l > 1.0 - kp.dbo_near) { aw[3] += 1.0; aw[4] += l; }
+      const int lpc = d.c_lp[c];
+      const int cls = (lpc >= 0 && d.lam[(size_t)r * kp.C + lpc] >= 0.5) ? 1 : 0;
+      double *ab = d.dbo_bar + ix * 4 + 2 * cls;
+      ab[0] += 1.0;
+      if (l > kp.dbo_trans_lo && l < kp.dbo_trans_hi) ab[1] += 1.0;
+    }
     if (!dyn && mode == 1) d.ti_sum[ix] += d.dvdl_coul[ix];   // <dV_coul/dlambda>
     if (!(fabs(l) <= 10.0) || !isfinite(dv)) atomicOr(&d.flags[FLAG_DIVERGED], 1);
   }
   kel = block_sum_d(kel);
   if (threadIdx.x == 0) {
-    if (frame) d.frame_total[r] += 1;
+    if (frame) {
+      d.frame_step[(size_t)r * kp.fcap + fslot] = m;
+      d.frame_total[r] += 1;
+    }
     if (energy) {
       double *e = d.erec + ((size_t)(m & 1) * kp.R + r) * kNE;
       e[CPH_E_SELF] = -f * kp.beta_d / sqrtpi * Q2;

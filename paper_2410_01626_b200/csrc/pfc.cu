@@ -1,11 +1,13 @@
 // Host-side Partition Function Correction (R2, R6).
 //
+// Recomputed after every DBO adjustment with the shifted knots.
 // Z_prot = int_{lp<0.5} e^{-beta V}, Z_deprot = int_{lp>=0.5} e^{-beta V} over the whole
 // wall-bounded range, V = Vdw + VpH (Vmm excluded).  The lambda=1 well depth d1
 // is solved so that G_deprot - G_prot = ln10 kT (pKa - pH) (bisection); His-like sites solve
 // (d1_p, d1_t) for the two micro free energies (Newton).  Targets out of reach of the single
 // well-depth correction saturate at +-80 kJ/mol (R22).  Composite Gauss-Legendre quadrature
 // with panels split at the spline knots and wall onsets, where the integrand is analytic.
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -51,34 +53,41 @@ struct Nodes {
   std::vector<double> x, w;
 };
 
-// Panels end at the spline knots and wall onsets (the integrand is analytic inside); the
-// steep quartic-wall intervals get more sub-panels.  Beyond -0.35 / 1.35 the integrand is
-// below 1e-30 of its peak.
-Nodes make_nodes(int sub, int order) {
-  static const double brk[] = {-0.35, -0.1, 0.0, 0.5, 1.0, 1.1, 1.35};
-  static const int wsub[] = {3, 1, 2, 2, 1, 3};
+// Panels end at the spline knots (the DBO well centres a0, a1 and the barrier position
+// (a0+a1)/2 of the coordinate), the smoothstep ends 0 and 1 of a protonation-keyed
+// tautomer barrier, the half-space split 0.5 and the wall onsets -0.1 / 1.1: the integrand
+// is analytic inside each.  Interior intervals get ~4*sub panels per unit length (at least
+// sub), the steep quartic-wall intervals 3*sub.  Beyond -0.35 / 1.35 the integrand is below
+// 1e-30 of its peak.
+Nodes make_nodes(int sub, int order, double a0, double a1) {
+  std::vector<double> brk = {-0.35, -0.1, 0.0, 0.5, 1.0, 1.1, 1.35, a0, a1, 0.5 * (a0 + a1)};
+  std::sort(brk.begin(), brk.end());
+  std::vector<double> b;
+  for (double v : brk)
+    if (b.empty() || v - b.back() > 1e-12) b.push_back(v);
   std::vector<double> gx, gw;
   gauss_legendre(order, gx, gw);
   Nodes nd;
-  for (int b = 0; b + 1 < (int)(sizeof(brk) / sizeof(brk[0])); ++b) {
-    const double a0 = brk[b], a1 = brk[b + 1];
-    const int nsub = sub * wsub[b];
+  for (size_t k = 0; k + 1 < b.size(); ++k) {
+    const double lo = b[k], hi = b[k + 1];
+    const bool wall = hi <= -0.1 + 1e-12 || lo >= 1.1 - 1e-12;
+    const int nsub = wall ? 3 * sub : std::max(sub, (int)std::ceil((hi - lo) * 4.0 * sub - 1e-9));
     for (int s = 0; s < nsub; ++s) {
-      const double c = a0 + (a1 - a0) * s / nsub, e = a0 + (a1 - a0) * (s + 1) / nsub;
-      for (int k = 0; k < order; ++k) {
-        nd.x.push_back(0.5 * (e - c) * gx[k] + 0.5 * (e + c));
-        nd.w.push_back(0.5 * (e - c) * gw[k]);
+      const double c = lo + (hi - lo) * s / nsub, e = lo + (hi - lo) * (s + 1) / nsub;
+      for (int q = 0; q < order; ++q) {
+        nd.x.push_back(0.5 * (e - c) * gx[q] + 0.5 * (e + c));
+        nd.w.push_back(0.5 * (e - c) * gw[q]);
       }
     }
   }
   return nd;
 }
 
-double free_energy_2state(const Nodes &nd, double h, double d1, double g, double kT, double kw) {
+double free_energy_2state(const Nodes &nd, const double dw[4], double d1, double g, double kT, double kw) {
   double zp = 0.0, zd = 0.0;
   for (size_t k = 0; k < nd.x.size(); ++k) {
     double v, dv;
-    vdw_eval(nd.x[k], h, d1, kw, &v, &dv);
+    vdw_eval(nd.x[k], dw[0], dw[1], dw[2], d1, kw, &v, &dv, nullptr);
     const double b = nd.w[k] * std::exp(-(v + nd.x[k] * g) / kT);
     if (nd.x[k] < 0.5) zp += b; else zd += b;
   }
@@ -104,44 +113,59 @@ double root_or_bound(F f) {
   return 0.5 * (lo + hi);
 }
 
-bool pfc_two_state(double h, double pKa, double pH, double T, double kw, double *d1, std::string *err) {
-  static const Nodes nd = make_nodes(6, 24);
+bool pfc_two_state(const double dw[4], double pKa, double pH, double T, double kw, double *d1, std::string *err) {
+  const Nodes nd = make_nodes(6, 24, dw[0], dw[1]);
   const double kT = kBoltz * T;
   const double target = delta_g(pKa, pH, T);
-  *d1 = root_or_bound([&](double x) { return free_energy_2state(nd, h, x, target, kT, kw) - target; });
+  *d1 = root_or_bound([&](double x) { return free_energy_2state(nd, dw, x, target, kT, kw) - target; });
   (void)err;
   return true;
 }
 
-bool pfc_three_state(double h, const double pKa3[3], double pH, double T, double kw, double *d1p,
-                     double *d1t, std::string *err) {
-  static const Nodes nd = make_nodes(2, 20);
-  const int n = (int)nd.x.size();
+// V_t(lt; h, d1) = h U(lt) + d1 W(lt) + walls(lt) (linear in h and d1): the protonation-keyed
+// tautomer barrier h(lp) enters through exp(-h(lp) U(lt) / kT), tabulated once per solve.
+bool pfc_three_state(const double dwp[4], const double dwt[4], const double pKa3[3], double pH, double T,
+                     double kw, double *d1p, double *d1t, std::string *err) {
+  const Nodes np_ = make_nodes(2, 20, dwp[0], dwp[1]);
+  const Nodes nt = make_nodes(2, 20, dwt[0], dwt[1]);
+  const int n = (int)np_.x.size(), m = (int)nt.x.size();
   const double kT = kBoltz * T;
   const double gd = delta_g(pKa3[1], pH, T), ge = delta_g(pKa3[2], pH, T);
-  // coupling kernel of VpH = lp [(1-lt) gd + lt ge]
-  std::vector<double> Kpt((size_t)n * n);
-  for (int p = 0; p < n; ++p)
-    for (int t = 0; t < n; ++t)
-      Kpt[(size_t)p * n + t] = std::exp(-nd.x[p] * ((1.0 - nd.x[t]) * gd + nd.x[t] * ge) / kT);
-  std::vector<double> a(n), b(n);
+  std::vector<double> U(m), Wd(m), Wall(m);
+  for (int t = 0; t < m; ++t) {
+    double v0, v1, v2, dv;
+    vdw_eval(nt.x[t], dwt[0], dwt[1], 0.0, 0.0, kw, &v0, &dv, nullptr);
+    vdw_eval(nt.x[t], dwt[0], dwt[1], 1.0, 0.0, kw, &v1, &dv, nullptr);
+    vdw_eval(nt.x[t], dwt[0], dwt[1], 0.0, 1.0, kw, &v2, &dv, nullptr);
+    Wall[t] = v0;
+    U[t] = v1 - v0;
+    Wd[t] = v2 - v0;
+  }
+  // M[p][t] = exp(-(h(lp) U(lt) + VpH(lp, lt)) / kT), VpH = lp [(1-lt) gd + lt ge]
+  std::vector<double> M((size_t)n * m);
+  for (int p = 0; p < n; ++p) {
+    double h, dh;
+    tautomer_barrier(np_.x[p], dwt[2], dwt[3], &h, &dh);
+    for (int t = 0; t < m; ++t)
+      M[(size_t)p * m + t] = std::exp(-(h * U[t] + np_.x[p] * ((1.0 - nt.x[t]) * gd + nt.x[t] * ge)) / kT);
+  }
+  std::vector<double> a(n), b(m);
   auto quad = [&](double dp, double dt, double out[2]) {
     for (int k = 0; k < n; ++k) {
       double v, dv;
-      vdw_eval(nd.x[k], h, dp, kw, &v, &dv);
-      a[k] = nd.w[k] * std::exp(-v / kT);
-      vdw_eval(nd.x[k], h, dt, kw, &v, &dv);
-      b[k] = nd.w[k] * std::exp(-v / kT);
+      vdw_eval(np_.x[k], dwp[0], dwp[1], dwp[2], dp, kw, &v, &dv, nullptr);
+      a[k] = np_.w[k] * std::exp(-v / kT);
     }
+    for (int t = 0; t < m; ++t) b[t] = nt.w[t] * std::exp(-(dt * Wd[t] + Wall[t]) / kT);
     double zp = 0.0, zdl = 0.0, zep = 0.0;
     for (int p = 0; p < n; ++p) {
       double s_lo = 0.0, s_hi = 0.0;
-      const double *row = &Kpt[(size_t)p * n];
-      for (int t = 0; t < n; ++t) {
+      const double *row = &M[(size_t)p * m];
+      for (int t = 0; t < m; ++t) {
         const double c = b[t] * row[t];
-        if (nd.x[t] < 0.5) s_lo += c; else s_hi += c;
+        if (nt.x[t] < 0.5) s_lo += c; else s_hi += c;
       }
-      if (nd.x[p] < 0.5) zp += a[p] * (s_lo + s_hi);
+      if (np_.x[p] < 0.5) zp += a[p] * (s_lo + s_hi);
       else { zdl += a[p] * s_lo; zep += a[p] * s_hi; }
     }
     out[0] = -kT * std::log(zdl / zp) - gd;

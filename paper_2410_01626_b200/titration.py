@@ -45,10 +45,14 @@ def gather_frames(local: np.ndarray, group=None, device=None):
     return np.concatenate([out[k, : counts[k]] for k in range(world)], 0)
 
 
-def deprotonated_fraction(lambda_p_frames) -> float:
+def deprotonated_fraction(lambda_p_frames, censored=None) -> float:
+    """x = N_deprot / N over the frames (deprotonated iff lambda_p >= 0.5, PAPER.md:979);
+    frames flagged by DBO censoring are left out."""
     lp = np.asarray(lambda_p_frames, np.float64)
+    if censored is not None:
+        lp = lp[~np.asarray(censored, bool)]
     if lp.size == 0 or not np.all(np.isfinite(lp)):
-        raise ValueError("need finite lambda frames")
+        raise ValueError("need finite, uncensored lambda frames")
     return float(np.count_nonzero(lp >= 0.5)) / lp.size
 
 

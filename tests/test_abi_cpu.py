@@ -68,3 +68,26 @@ def test_invalid_params_rejected(cph):
     with pytest.raises(cph.CphError) as ei:
         cph.cph_create(s, [np.nan], [1], use_torch_allocator=False)
     assert ei.value.status == 1
+
+
+def test_dbo_defaults_are_the_papers(cph):
+    """cph_default_params carries the DBO constants of PAPER.md:778-798 (off by default)."""
+    import ctypes
+    p = cph.binding.cph_params()
+    cph.lib().cph_default_params(ctypes.byref(p))
+    assert p.abi_version == 2 and p.dbo_well == 0 and p.dbo_barrier == 0
+    assert (p.dbo_well_steps, p.dbo_barrier_steps, p.dbo_censor_steps) == (20000, 500000, 5000)   # 40 ps, 1 ns, 10 ps
+    assert (p.dbo_well_near, p.dbo_residency, p.dbo_well_tol, p.dbo_well_gain, p.dbo_well_cap) == (0.2, 0.7, 0.03, 0.5, 0.08)
+    assert (p.dbo_trans_lo, p.dbo_trans_hi, p.dbo_target, p.dbo_target_tol) == (0.2, 0.8, 0.25, 0.05)
+    assert (p.dbo_barrier_step, p.dbo_barrier_min, p.dbo_barrier_max, p.barrier) == (1.0, 1.0, 20.0, 6.0)
+
+
+def test_invalid_dbo_params_rejected(cph):
+    s = _sys()
+    for kw in (dict(dbo_well=1, dbo_well_steps=15),            # not a multiple of nstlist = 10
+               dict(dbo_barrier=1, dbo_barrier_steps=0),
+               dict(dbo_well=1, dbo_well_cap=0.5),
+               dict(dbo_barrier=1, dbo_barrier_min=5.0, dbo_barrier_max=2.0)):
+        with pytest.raises(cph.CphError) as ei:
+            cph.cph_create(s, [4.0], [1], use_torch_allocator=False, **kw)
+        assert ei.value.status == 1 and "DBO" in str(ei.value), kw

@@ -50,6 +50,8 @@ def test_assign_replicas_round_robin():
 
 def test_fraction_and_fits_match_oracle():
     assert T.deprotonated_fraction([0.5, 0.49, 0.9, 0.1]) == 0.5          # lambda_p >= 0.5 (R1)
+    # censored frames (DBO) do not count
+    assert T.deprotonated_fraction([0.5, 0.49, 0.9, 0.1], censored=[0, 0, 1, 0]) == 1 / 3
     rng = np.random.default_rng(3)
     pH = np.repeat(np.linspace(2.0, 8.0, 13), 4)
     x = np.clip(OA.hh(pH, 4.4, 0.9) + rng.normal(0, 0.02, pH.size), 0, 1)
