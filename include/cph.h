@@ -14,7 +14,8 @@
  *       lambda-group, plus the bias V = Vmm + VpH + Vdw (Eq. 3, PAPER.md:667-698,
  *       :715-740).
  *   a9  BAOAB Langevin / velocity-Verlet update of atoms and lambda particles
- *       (m_lambda = 60 u), dt = 2 fs, 300 K.
+ *       (m_lambda = 60 u), dt = 2 fs, 300 K;
+ *   f2  or, instead of the Langevin O step, the paper's Bussi thermostat.
  *   a10 Partition Function Correction of the double-well depths at cph_create /
  *       cph_set_pH.
  *   f1  optional Dynamic Barrier and Well Optimization with censoring
@@ -155,6 +156,14 @@ typedef struct {
   double dbo_barrier_step;      /* 1.0 kJ/mol */
   double dbo_barrier_min;       /* 1 kJ/mol */
   double dbo_barrier_max;       /* 20 kJ/mol */
+  /* Thermostat: 0 = Langevin BAOAB with gamma_atom / gamma_lambda (default);
+   * 1 = Bussi-Donadio-Parrinello velocity rescaling as in the paper (PAPER.md:888,
+   * :902-906), one group per replica for the atoms (3 x mobile atoms degrees of
+   * freedom) and one for its lambda particles (C degrees of freedom), applied in the
+   * middle of the step in place of the Langevin O step (R27, R28). */
+  int32_t thermostat;
+  double tau_atom;              /* ps (0.1) */
+  double tau_lambda;            /* ps (1.0) */
 } cph_params;
 
 /* DBO event kinds (cph_dbo_event.kind) */

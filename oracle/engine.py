@@ -9,6 +9,9 @@ Follows, in order:
   * BAOAB (reading R9; velocity Verlet PAPER.md:896 + stochastic thermostat
     PAPER.md:902-907): B v+=dt/2 F/m; A x+=dt/2 v; O v=c1 v+sqrt((1-c1^2)kT/m) xi;
     A x+=dt/2 v; forces at (x, lambda) jointly; B v+=dt/2 F/m; c1 = exp(-gamma dt).
+    With params thermostat="bussi" the O step is the Bussi velocity rescaling of the
+    group (atoms tau_atom = 0.1 ps, lambda tau_lambda = 1 ps; PAPER.md:888, :902-906;
+    oracle.thermostat, readings R27/R28).
     Atoms: m from the system, mass 0 = frozen.  lambda: m = 60 u,
     gamma = 1/tau = 1 ps^-1.  Noise from oracle.philox.
   * Partition Function Correction at construction.
@@ -24,6 +27,7 @@ import numpy as np
 from . import bias as B
 from . import dbo as DBO
 from . import pfc as PFC
+from . import thermostat as TH
 from .charges import charges, coord_ptr
 from .ewald import (ewald_beta, exclusion_correction, net_charge_term, real_space,
                     recip_direct, self_term)
@@ -188,24 +192,37 @@ class OracleReplica:
         n = self.step_index
         m = np.where(self.mobile, self.mass, 1.0)[:, None]
         mob = self.mobile[:, None]
-        c1 = math.exp(-p["gamma_atom"] * h)
-        sd = np.sqrt((1.0 - c1 * c1) * kt / m)
-        xi = normals(self.seed, n, np.arange(len(self.x)), 0)[:, :3]
+        bussi = p.get("thermostat", "langevin") == "bussi"
         F = self.cur["F"]
         v = self.v + np.where(mob, 0.5 * h * F / m, 0.0)                  # B
         x = self.x + np.where(mob, 0.5 * h * v, 0.0)                      # A
-        v = np.where(mob, c1 * v + sd * xi, 0.0)                          # O
+        if bussi:                                                         # O: Bussi rescale
+            nf = 3 * int(np.count_nonzero(self.mobile))
+            K = 0.5 * float(np.sum(np.where(mob, m * v * v, 0.0)))
+            R1, S = TH.bussi_draws(self.seed, n, TH.STREAM_ATOMS, nf)
+            v = TH.bussi_alpha(K, nf, kt, h, p.get("tau_atom", 0.1), R1, S) * v
+        else:                                                             # O: Langevin
+            c1 = math.exp(-p["gamma_atom"] * h)
+            sd = np.sqrt((1.0 - c1 * c1) * kt / m)
+            xi = normals(self.seed, n, np.arange(len(self.x)), 0)[:, :3]
+            v = np.where(mob, c1 * v + sd * xi, 0.0)
         x = x + np.where(mob, 0.5 * h * v, 0.0)                           # A
         lam, lamv = self.lam, self.lamv
         if not self.fixed_lambda:
             ml = p["lambda_mass"]
-            cl = math.exp(-p["gamma_lambda"] * h)
-            sdl = math.sqrt((1.0 - cl * cl) * kt / ml)
-            xil = normals(self.seed, n, np.arange(len(lam)), 1)[:, 0]
             Fl = -(self.cur["dvdl_coul"] + self.cur["dvdl_bias"])
             lamv = lamv + 0.5 * h * Fl / ml
             lam = lam + 0.5 * h * lamv
-            lamv = cl * lamv + sdl * xil
+            if bussi:
+                nf = len(lam)
+                R1, S = TH.bussi_draws(self.seed, n, TH.STREAM_LAMBDA, nf)
+                lamv = TH.bussi_alpha(0.5 * ml * float(np.sum(lamv * lamv)), nf, kt, h,
+                                      p.get("tau_lambda", 1.0), R1, S) * lamv
+            else:
+                cl = math.exp(-p["gamma_lambda"] * h)
+                sdl = math.sqrt((1.0 - cl * cl) * kt / ml)
+                xil = normals(self.seed, n, np.arange(len(lam)), 1)[:, 0]
+                lamv = cl * lamv + sdl * xil
             lam = lam + 0.5 * h * lamv
         cur = self.evaluate(x, lam)                                       # forces at (x, lambda)
         v = v + np.where(mob, 0.5 * h * cur["F"] / m, 0.0)                # B

@@ -55,7 +55,8 @@ class cph_params(C.Structure):
                 ("dbo_residency", C.c_double), ("dbo_well_tol", C.c_double), ("dbo_well_gain", C.c_double),
                 ("dbo_well_cap", C.c_double), ("dbo_trans_lo", C.c_double), ("dbo_trans_hi", C.c_double),
                 ("dbo_target", C.c_double), ("dbo_target_tol", C.c_double), ("dbo_barrier_step", C.c_double),
-                ("dbo_barrier_min", C.c_double), ("dbo_barrier_max", C.c_double)]
+                ("dbo_barrier_min", C.c_double), ("dbo_barrier_max", C.c_double),
+                ("thermostat", C.c_int32), ("tau_atom", C.c_double), ("tau_lambda", C.c_double)]
 
 
 class cph_dbo_event(C.Structure):
@@ -212,9 +213,12 @@ def cph_create(system, pH, replica_seed, *, lambda0=None, pos_replicas=None, vel
               "dbo_well_steps", "dbo_barrier_steps", "dbo_censor_steps"):
         if k in params:
             setattr(p, k, int(params[k]))
-    for k in ("dbo_well_near", "dbo_residency", "dbo_well_tol", "dbo_well_gain", "dbo_well_cap", "dbo_trans_lo",
-              "dbo_trans_hi", "dbo_target", "dbo_target_tol", "dbo_barrier_step", "dbo_barrier_min",
-              "dbo_barrier_max"):
+    if "thermostat" in params:
+        t = params["thermostat"]
+        p.thermostat = {"langevin": 0, "bussi": 1}[t] if isinstance(t, str) else int(t)
+    for k in ("tau_atom", "tau_lambda", "dbo_well_near", "dbo_residency", "dbo_well_tol", "dbo_well_gain",
+              "dbo_well_cap", "dbo_trans_lo", "dbo_trans_hi", "dbo_target", "dbo_target_tol", "dbo_barrier_step",
+              "dbo_barrier_min", "dbo_barrier_max"):
         if k in params:
             setattr(p, k, float(params[k]))
     grid = overrides.get("pme_grid", getattr(system, "pme_grid", None))

@@ -54,6 +54,53 @@ __device__ inline double lambda_normal(uint64_t seed, uint32_t step, uint32_t co
 }
 
 // ---------------------------------------------------------------------------------
+// Bussi-Donadio-Parrinello velocity rescaling factor for one thermostat group
+// (R27/R28): R1 and the chi^2(Nf-1) sum S come from Philox counters
+// (step, k, stream, 0); S by explicit squares for Nf-1 <= 32, else 2 Gamma((Nf-1)/2)
+// by Marsaglia-Tsang.  K' = K + (1-c)(Kbar (R1^2+S)/Nf - K) + 2 R1 sqrt(K Kbar/Nf (1-c) c),
+// alpha = sgn(R1 + sqrt(c Nf K/((1-c) Kbar))) sqrt(K'/K), c = exp(-dt/tau).
+// ---------------------------------------------------------------------------------
+__device__ inline void philox_uniforms(uint64_t seed, uint32_t step, uint32_t k, uint32_t stream, double u[4]) {
+  const U4 o = philox4x32_10(U4{step, k, stream, 0u}, (uint32_t)seed, (uint32_t)(seed >> 32));
+  const double s = 2.3283064365386963e-10;
+  u[0] = ((double)o.x + 0.5) * s; u[1] = ((double)o.y + 0.5) * s;
+  u[2] = ((double)o.z + 0.5) * s; u[3] = ((double)o.w + 0.5) * s;
+}
+
+__device__ inline double bussi_alpha(uint64_t seed, uint32_t step, uint32_t stream, double K, int nf, double kT,
+                                     double c) {
+  if (nf <= 0 || !(K > 0.0)) return 1.0;
+  double u[4];
+  philox_uniforms(seed, step, 0u, stream, u);
+  const double R1 = sqrt(-2.0 * log(u[0])) * cospi(2.0 * u[1]);
+  const int m = nf - 1;
+  double S = 0.0;
+  if (m > 0 && m <= 32) {
+    for (int k = 1, left = m; left > 0; ++k) {
+      philox_uniforms(seed, step, (uint32_t)k, stream, u);
+      const double r0 = sqrt(-2.0 * log(u[0])), r1 = sqrt(-2.0 * log(u[2]));
+      const double z[4] = {r0 * cospi(2.0 * u[1]), r0 * sinpi(2.0 * u[1]), r1 * cospi(2.0 * u[3]),
+                           r1 * sinpi(2.0 * u[3])};
+      for (int q = 0; q < 4 && left > 0; ++q, --left) S += z[q] * z[q];
+    }
+  } else if (m > 32) {
+    const double d = 0.5 * m - 1.0 / 3.0, cc = 1.0 / sqrt(9.0 * d);
+    for (uint32_t k = 1;; ++k) {
+      philox_uniforms(seed, step, k, stream, u);
+      const double x = sqrt(-2.0 * log(u[0])) * cospi(2.0 * u[1]);
+      const double t = 1.0 + cc * x;
+      const double v = t * t * t;
+      if (v > 0.0 && log(u[2]) < 0.5 * x * x + d - d * v + d * log(v)) { S = 2.0 * d * v; break; }
+    }
+  }
+  const double kbar = 0.5 * nf * kT;
+  const double kn = K + (1.0 - c) * (kbar * (R1 * R1 + S) / nf - K) + 2.0 * R1 * sqrt(K * kbar / nf * (1.0 - c) * c);
+  double alpha = sqrt(fmax(kn, 0.0) / K);
+  if (c < 1.0 && R1 + sqrt(c * nf * K / ((1.0 - c) * kbar)) < 0.0) alpha = -alpha;
+  return alpha;
+}
+
+// ---------------------------------------------------------------------------------
 // erfc(z) = t P(t) exp(-z^2), t = 1/(1 + p z): least-squares-minimax fit of
 // erfcx(z)/t on z in [0, 4] (rel. error 3e-8 in exact arithmetic, 4e-7 in fp32).
 // exp(-z^2) is shared with the Ewald force term.

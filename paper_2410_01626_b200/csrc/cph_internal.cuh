@@ -68,6 +68,9 @@ struct KParams {
   // DBO statistics: on/off and the proximity / transition bands
   int dbo_on;
   double dbo_near, dbo_trans_lo, dbo_trans_hi;
+  // Bussi thermostat (R27/R28): on/off, degrees of freedom, exp(-dt/tau)
+  int bussi;
+  double nf_atom, cb_atom, cb_lam;
 };
 
 struct DevBufs {
@@ -115,6 +118,7 @@ struct DevBufs {
   long long *cens = nullptr;                        // [R*G*2] censor window (from, until]
   unsigned char *frame_cens = nullptr;              // [R*fcap*C]
   long long *frame_step = nullptr;                  // [R*fcap]
+  double *bussi_k = nullptr;                        // [2*R] mid-step atom kinetic energy by step parity
 };
 
 struct DboConfig {
@@ -161,7 +165,7 @@ struct Ctx {
 };
 
 // ---- launchers (each returns the number of kernels it launched) ----------------------
-int launch_integrate(Ctx &c, cudaStream_t s, int do_open);       // BAOA (+ pending close)
+int launch_integrate(Ctx &c, cudaStream_t s, int do_open);       // BAOA (+ pending close); Bussi: BA + T A
 int launch_close(Ctx &c, cudaStream_t s, int kick);                // final half kick / KE
 int launch_rebuild(Ctx &c, cudaStream_t s);                        // sort + pair list
 int launch_nonbonded(Ctx &c, cudaStream_t s, int step_offset);

@@ -196,6 +196,7 @@ cph_status evaluate_here(Ctx &c) {
   cudaStream_t s = c.stream;
   k_set_end<<<1, 1, 0, s>>>(c.d.end_step, c.host_step);
   CK(cudaMemsetAsync(c.d.erec + (size_t)(c.host_step & 1) * c.kp.R * kNE, 0, sizeof(double) * c.kp.R * kNE, s));
+  CK(cudaMemsetAsync(c.d.bussi_k, 0, sizeof(double) * 2 * c.kp.R, s));
   int k = 1;
   k += launch_set_charges(c, s);
   k += launch_rebuild(c, s);
@@ -296,6 +297,9 @@ void cph_default_params(cph_params *p) {
   p->dbo_barrier_step = 1.0;
   p->dbo_barrier_min = 1.0;
   p->dbo_barrier_max = 20.0;
+  p->thermostat = 0;
+  p->tau_atom = 0.1;
+  p->tau_lambda = 1.0;
 }
 
 const char *cph_last_error(const cph_ctx *ctx) { return ctx ? ctx->c.err.c_str() : g_create_err.c_str(); }
@@ -340,6 +344,9 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   if (prm->nstlist < 1 || prm->nstout < 1 || prm->nstenergy < 1 || prm->frame_capacity < 1)
     return bad("nstlist, nstout, nstenergy, frame_capacity must be >= 1");
   if (prm->mode != 0 && prm->mode != 1) return bad("mode must be 0 or 1");
+  if (prm->thermostat != 0 && prm->thermostat != 1) return bad("thermostat must be 0 (Langevin) or 1 (Bussi)");
+  if (prm->thermostat == 1 && !(prm->tau_atom > 0.0 && prm->tau_lambda > 0.0))
+    return bad("Bussi coupling times must be > 0");
   if (prm->dbo_well || prm->dbo_barrier) {
     if ((prm->dbo_well && (prm->dbo_well_steps < 1 || prm->dbo_well_steps % prm->nstlist)) ||
         (prm->dbo_barrier && (prm->dbo_barrier_steps < 1 || prm->dbo_barrier_steps % prm->nstlist)) ||
@@ -497,6 +504,14 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     kp.dbo_on = on ? 1 : 0;
     kp.dbo_near = b.near; kp.dbo_trans_lo = b.trans_lo; kp.dbo_trans_hi = b.trans_hi;
   }
+  kp.bussi = prm->thermostat == 1;
+  {
+    int mobile = 0;
+    for (int i = 0; i < N; ++i) mobile += sys->mass[i] > 0.0f;
+    kp.nf_atom = 3.0 * mobile;
+    kp.cb_atom = kp.bussi ? std::exp(-prm->dt / prm->tau_atom) : 1.0;
+    kp.cb_lam = kp.bussi ? std::exp(-prm->dt / prm->tau_lambda) : 1.0;
+  }
   kp.Q_fixed = 0.0; kp.Q2_fixed = 0.0;
   for (int i = 0; i < N; ++i)
     if (lslot[i] < 0) { kp.Q_fixed += sys->charge[i]; kp.Q2_fixed += (double)sys->charge[i] * sys->charge[i]; }
@@ -570,6 +585,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   d.cens = dalloc<long long>(c, (size_t)R * G * 2);
   d.frame_cens = dalloc<unsigned char>(c, (size_t)R * kp.fcap * C);
   d.frame_step = dalloc<long long>(c, (size_t)R * kp.fcap);
+  d.bussi_k = dalloc<double>(c, 2 * (size_t)R);
   for (void *p : {(void *)d.xyzq, (void *)d.nbl, (void *)d.grid, (void *)d.cgrid, (void *)d.flags, (void *)d.seed})
     if (!p) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
   if (c.allocations.size() < 40) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }

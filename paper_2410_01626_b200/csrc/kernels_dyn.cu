@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(128) k_integrate(KParams kp, DevBufs d) {
   const int pending = d.flags[FLAG_PENDING_CLOSE];
   if (blockIdx.x == 0 && threadIdx.x < kNE)   // record of step n+1 starts empty
     d.erec[((size_t)((n + 1) & 1) * kp.R + r) * kNE + threadIdx.x] = 0.0;
-  double ke = 0.0;
+  double ke = 0.0, kmid = 0.0;
   if (i < kp.N) {
     const size_t idx = (size_t)r * kp.Nst + i;
     float4 v = d.vel[idx];
@@ -33,6 +33,14 @@ __global__ void __launch_bounds__(128) k_integrate(KParams kp, DevBufs d) {
       v.x = fmaf(hk, fx, v.x); v.y = fmaf(hk, fy, v.y); v.z = fmaf(hk, fz, v.z);      // B
       const float hdt = 0.5f * kp.dt;
       x.x = fmaf(hdt, v.x, x.x); x.y = fmaf(hdt, v.y, x.y); x.z = fmaf(hdt, v.z, x.z);  // A
+      if (kp.bussi) {
+        // Bussi: the group's mid-step kinetic energy is reduced here; k_thermo rescales
+        // and applies the second A (R27)
+        kmid = 0.5 * ((double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z) / invm;
+        d.xyzq[idx] = x;
+        d.vel[idx] = v;
+        goto done;
+      }
       const int orig = d.meta[idx].x;
       const float3 xi = atom_normals(d.seed[r], (uint32_t)n, (uint32_t)orig);
       const float sd = sqrtf(kp.c2_atom_kT * invm);
@@ -44,8 +52,38 @@ __global__ void __launch_bounds__(128) k_integrate(KParams kp, DevBufs d) {
       d.vel[idx] = v;
     }
   }
+done:
   if (pending && is_energy_step(n, end, kp.nstenergy))
     block_atomic_add_d(ke, &d.erec[((size_t)(n & 1) * kp.R + r) * kNE + CPH_E_KE_ATOMS]);
+  if (kp.bussi) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.bussi_k[((n + 1) & 1) * kp.R + r] = 0.0;   // next step's sum
+    block_atomic_add_d(kmid, &d.bussi_k[(n & 1) * kp.R + r]);
+  }
+}
+
+// Bussi step for the atoms of every replica: alpha from the reduced mid-step kinetic energy
+// (computed once per CTA), v *= alpha, then the second A
+__global__ void __launch_bounds__(128) k_thermo(KParams kp, DevBufs d) {
+  const int r = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long n = *d.step;
+  __shared__ double s_alpha;
+  if (threadIdx.x == 0)
+    s_alpha = bussi_alpha(d.seed[r], (uint32_t)n, 2u, d.bussi_k[(n & 1) * kp.R + r], (int)kp.nf_atom, kp.kT,
+                          kp.cb_atom);
+  __syncthreads();
+  if (i >= kp.N) return;
+  const size_t idx = (size_t)r * kp.Nst + i;
+  float4 v = d.vel[idx];
+  if (v.w > 0.0f) {
+    const float a = (float)s_alpha;
+    v.x *= a; v.y *= a; v.z *= a;
+    float4 x = d.xyzq[idx];
+    const float hdt = 0.5f * kp.dt;
+    x.x = fmaf(hdt, v.x, x.x); x.y = fmaf(hdt, v.y, x.y); x.z = fmaf(hdt, v.z, x.z);  // A
+    d.xyzq[idx] = x;
+    d.vel[idx] = v;
+  }
 }
 
 // closing half kick (kick = 1) and/or kinetic energy of the current velocities
@@ -88,19 +126,37 @@ __device__ void lambda_set_charges(const KParams &kp, const DevBufs &d, int r) {
   }
 }
 
+__device__ double block_sum_d(double v);
+
 // BAOA for lambda coordinates of replica r with noise index `step`, then new charges
+// (O = Langevin, or the Bussi rescaling of the replica's lambda group, R27)
 __device__ void lambda_open(const KParams &kp, const DevBufs &d, int r, long long step) {
+  const double h = kp.dtd;
+  double ke = 0.0;
   for (int c = threadIdx.x; c < kp.C; c += blockDim.x) {
     const size_t ix = (size_t)r * kp.C + c;
     const double F = -(d.dvdl_coul[ix] + d.dvdl_bias[ix]);
-    const double h = kp.dtd;
     double v = d.lamv[ix], l = d.lam[ix];
     v += 0.5 * h * F / kp.m_lam;                                              // B
     l += 0.5 * h * v;                                                         // A
-    v = kp.c1_lam * v + kp.sd_lam * lambda_normal(d.seed[r], (uint32_t)step, (uint32_t)c);  // O
-    l += 0.5 * h * v;                                                         // A
+    if (kp.bussi) {
+      ke += 0.5 * kp.m_lam * v * v;
+    } else {
+      v = kp.c1_lam * v + kp.sd_lam * lambda_normal(d.seed[r], (uint32_t)step, (uint32_t)c);  // O
+      l += 0.5 * h * v;                                                       // A
+    }
     d.lamv[ix] = v;
     d.lam[ix] = l;
+  }
+  if (kp.bussi) {
+    const double K = block_sum_d(ke);
+    const double alpha = bussi_alpha(d.seed[r], (uint32_t)step, 3u, K, kp.C, kp.kT, kp.cb_lam);
+    for (int c = threadIdx.x; c < kp.C; c += blockDim.x) {
+      const size_t ix = (size_t)r * kp.C + c;
+      const double v = alpha * d.lamv[ix];                                    // O (Bussi)
+      d.lamv[ix] = v;
+      d.lam[ix] += 0.5 * h * v;                                               // A
+    }
   }
   __syncthreads();
   lambda_set_charges(kp, d, r);
@@ -289,7 +345,9 @@ __global__ void __launch_bounds__(256) k_set_charges(KParams kp, DevBufs d) {
 int launch_integrate(Ctx &c, cudaStream_t s, int) {
   dim3 grid((c.kp.N + 127) / 128, c.kp.R);
   k_integrate<<<grid, 128, 0, s>>>(c.kp, c.d);
-  return 1;
+  if (!c.kp.bussi) return 1;
+  k_thermo<<<grid, 128, 0, s>>>(c.kp, c.d);
+  return 2;
 }
 int launch_close(Ctx &c, cudaStream_t s, int kick) {
   dim3 grid((c.kp.N + 127) / 128, c.kp.R);
