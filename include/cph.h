@@ -164,6 +164,16 @@ typedef struct {
   int32_t thermostat;
   double tau_atom;              /* ps (0.1) */
   double tau_lambda;            /* ps (1.0) */
+  /* pH replica exchange (SURVEY §8(f) f3; the paper's outlook, PAPER.md:1664, :1738;
+   * DESIGN.md R29, R30).  Replicas of all contexts taking part (one per GPU) form
+   * remd_total / n_ph_levels ladders in global order (global replica g = remd_first + r
+   * belongs to ladder g / n_ph_levels); every replica's pH must be one of ph_levels and
+   * the labels inside a ladder a permutation of the levels.  Not combinable with DBO
+   * or fixed-lambda mode (CPH_E_UNSUPPORTED). */
+  int32_t n_ph_levels;          /* P >= 2 enables exchange; 0 = off */
+  const double *ph_levels;      /* [P] strictly ascending pH levels */
+  int32_t remd_first;           /* global index of this context's replica 0 (0) */
+  int32_t remd_total;           /* replicas over all contexts, multiple of P (0 = R) */
 } cph_params;
 
 /* DBO event kinds (cph_dbo_event.kind) */
@@ -223,12 +233,15 @@ cph_status cph_get_bias_params(cph_ctx *ctx, int32_t replica, double *d1 /*[C]*/
  * dropped oldest-first and *n_dropped reports how many. */
 cph_status cph_get_frames(cph_ctx *ctx, int32_t replica, float *buf, int64_t cap,
                           int64_t *n_frames, int64_t *n_dropped);
-/* As cph_get_frames, plus per frame the step it was taken at (steps [cap] or NULL)
+/* As cph_get_frames, plus per frame the step it was taken at (steps [cap] or NULL),
+ * the pH level index the replica simulated then (labels [cap] or NULL; -1 without
+ * replica exchange)
  * and per frame and coordinate a censor flag (censored [cap*C] or NULL): 1 iff the
  * coordinate's site had a DBO adjustment at a block end S with
  * S < step <= S + dbo_censor_steps (R26). */
 cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t replica, float *buf, uint8_t *censored,
-                             int64_t *steps, int64_t cap, int64_t *n_frames, int64_t *n_dropped);
+                             int64_t *steps, int32_t *labels, int64_t cap, int64_t *n_frames,
+                             int64_t *n_dropped);
 /* DBO parameters per coordinate [C*4]: (a0, a1, h_prot, h_deprot) = well centres of
  * the lambda = 0 and lambda = 1 wells, and the barrier heights (kJ/mol).  lambda_p
  * coordinates use h_prot == h_deprot; a tautomer coordinate's barrier is
@@ -249,6 +262,28 @@ cph_status cph_get_dbo_events(cph_ctx *ctx, cph_dbo_event *ev, int64_t cap, int6
  * lambda_p coordinates / protonated frames for tautomer coordinates, B =
  * deprotonated frames.  Either pointer may be NULL. */
 cph_status cph_get_dbo_stats(cph_ctx *ctx, int32_t replica, double *well, double *barrier);
+
+/* pH replica exchange (n_ph_levels >= 2).  One attempt = cph_exchange_energies on every
+ * context, the rows of all contexts concatenated in global replica order (an NCCL
+ * all-gather across GPUs), then cph_exchange_apply on every context with the same seed
+ * and attempt index: each applies all Metropolis decisions (identical everywhere) to its
+ * own replicas and re-evaluates their bias forces.  Call between cph_step calls.
+ * rows / rows_all are DEVICE pointers on the context's device; the work is enqueued on
+ * the context stream (no host synchronisation).
+ * cph_exchange_energies: rows [R*(P+1)] = (label, E_0 .. E_{P-1}) per local replica,
+ *   E_p = pH-dependent bias (VpH + Vdw at level p's PFC depths), kJ/mol, fp64.
+ * cph_exchange_apply: rows_all [remd_total*(P+1)]; pairs (p, p+1), p = attempt mod 2,
+ *   +2, ...; accept with min(1, exp(-Delta/kT)), u from Philox(seed; attempt, ladder, p, 5). */
+cph_status cph_exchange_energies(cph_ctx *ctx, double *rows);
+cph_status cph_exchange_apply(cph_ctx *ctx, const double *rows_all, uint64_t seed, int64_t attempt);
+/* Single-context shortcut (remd_total == R): energies + apply on an internal buffer. */
+cph_status cph_exchange(cph_ctx *ctx, uint64_t seed, int64_t attempt);
+/* Current level index per local replica [R] (synchronizes), and restart setter. */
+cph_status cph_get_labels(cph_ctx *ctx, int32_t *labels);
+cph_status cph_set_labels(cph_ctx *ctx, const int32_t *labels);
+/* Attempts and accepted swaps per ladder and level pair [L*(P-1)], L = remd_total/P
+ * (every context counts every ladder). */
+cph_status cph_get_exchange_stats(cph_ctx *ctx, int64_t *attempts, int64_t *accepts);
 
 /* Force on every atom [3N] (kJ mol^-1 nm^-1) and the full electrostatic potential
  * phi_i = (1/f) dE_coul/dq_i [N] (e/nm; real + exclusion + reciprocal + self +

@@ -56,7 +56,9 @@ class cph_params(C.Structure):
                 ("dbo_well_cap", C.c_double), ("dbo_trans_lo", C.c_double), ("dbo_trans_hi", C.c_double),
                 ("dbo_target", C.c_double), ("dbo_target_tol", C.c_double), ("dbo_barrier_step", C.c_double),
                 ("dbo_barrier_min", C.c_double), ("dbo_barrier_max", C.c_double),
-                ("thermostat", C.c_int32), ("tau_atom", C.c_double), ("tau_lambda", C.c_double)]
+                ("thermostat", C.c_int32), ("tau_atom", C.c_double), ("tau_lambda", C.c_double),
+                ("n_ph_levels", C.c_int32), ("ph_levels", _f64p), ("remd_first", C.c_int32),
+                ("remd_total", C.c_int32)]
 
 
 class cph_dbo_event(C.Structure):
@@ -83,7 +85,14 @@ EXPORTS = {
     "cph_get_energies": (C.c_int, [C.c_void_p, C.c_int32, _f64p]),
     "cph_get_bias_params": (C.c_int, [C.c_void_p, C.c_int32, _f64p]),
     "cph_get_frames": (C.c_int, [C.c_void_p, C.c_int32, _f32p, C.c_int64, _i64p, _i64p]),
-    "cph_get_frames_ex": (C.c_int, [C.c_void_p, C.c_int32, _f32p, _p(C.c_uint8), _i64p, C.c_int64, _i64p, _i64p]),
+    "cph_get_frames_ex": (C.c_int, [C.c_void_p, C.c_int32, _f32p, _p(C.c_uint8), _i64p, _i32p, C.c_int64, _i64p,
+                                    _i64p]),
+    "cph_exchange_energies": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "cph_exchange_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int64]),
+    "cph_exchange": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int64]),
+    "cph_get_labels": (C.c_int, [C.c_void_p, _i32p]),
+    "cph_set_labels": (C.c_int, [C.c_void_p, _i32p]),
+    "cph_get_exchange_stats": (C.c_int, [C.c_void_p, _i64p, _i64p]),
     "cph_get_dbo_params": (C.c_int, [C.c_void_p, C.c_int32, _f64p]),
     "cph_set_dbo_params": (C.c_int, [C.c_void_p, C.c_int32, _f64p]),
     "cph_get_dbo_events": (C.c_int, [C.c_void_p, _p(cph_dbo_event), C.c_int64, _i64p]),
@@ -155,9 +164,11 @@ def _torch_allocator(device):
 
 
 def cph_create(system, pH, replica_seed, *, lambda0=None, pos_replicas=None, vel_replicas=None, device=0,
-               mode=0, cuda_stream=None, use_torch_allocator=True, **overrides):
+               mode=0, cuda_stream=None, use_torch_allocator=True, ph_levels=None, remd_first=0, remd_total=0,
+               **overrides):
     """Create a context for R = len(pH) replicas of `system` (any object with the
-    SyntheticSystem attributes).  Parameter overrides use cph_params field names."""
+    SyntheticSystem attributes).  Parameter overrides use cph_params field names.
+    ph_levels (sorted pH values) enables pH replica exchange."""
     L = lib()
     pH = np.ascontiguousarray(pH, np.float64).reshape(-1)
     R = len(pH)
@@ -229,6 +240,12 @@ def cph_create(system, pH, replica_seed, *, lambda0=None, pos_replicas=None, vel
     p.lambda0 = _ptr(arr(lambda0, np.float64), C.c_double)
     p.pos_replicas = _ptr(arr(pos_replicas, np.float32), C.c_float)
     p.vel_replicas = _ptr(arr(vel_replicas, np.float32), C.c_float)
+    if ph_levels is not None:
+        lv = arr(ph_levels, np.float64).reshape(-1)
+        p.n_ph_levels = len(lv)
+        p.ph_levels = _ptr(lv, C.c_double)
+        p.remd_first = int(remd_first)
+        p.remd_total = int(remd_total)
     p.cuda_stream = cuda_stream
     cbs = None
     if use_torch_allocator:
@@ -245,15 +262,17 @@ def cph_create(system, pH, replica_seed, *, lambda0=None, pos_replicas=None, vel
             cbs = None
     h = C.c_void_p()
     _check(L.cph_create(C.byref(s), C.byref(p), C.byref(h)))
-    return Context(h, R, cbs)
+    return Context(h, R, cbs, p.n_ph_levels, device)
 
 
 class Context:
     """Owns a cph_ctx handle; methods are the cph_* getters with numpy outputs."""
 
-    def __init__(self, handle, R, callbacks):
+    def __init__(self, handle, R, callbacks, n_levels=0, device=0):
         self.h = handle
         self.R = R
+        self.P = n_levels
+        self.device = device
         self._cbs = callbacks            # keep allocator callbacks alive
         self.C = lib().cph_n_coords(handle)
         self.N = lib().cph_n_atoms(handle)
@@ -314,17 +333,59 @@ class Context:
         return buf[: n.value * self.C].reshape(n.value, self.C), dropped.value
 
     def cph_get_frames_ex(self, r, cap=1 << 20):
-        """(frames [n, C], censored [n, C] bool, steps [n], n_dropped)."""
+        """(frames [n, C], censored [n, C] bool, steps [n], pH-level labels [n], n_dropped)."""
         cap = int(cap)
         buf = np.zeros(max(cap, 1) * max(self.C, 1), np.float32)
         cen = np.zeros(max(cap, 1) * max(self.C, 1), np.uint8)
         st = np.zeros(max(cap, 1), np.int64)
+        lab = np.zeros(max(cap, 1), np.int32)
         n, dropped = C.c_int64(), C.c_int64()
         _check(lib().cph_get_frames_ex(self.h, r, _ptr(buf, C.c_float), _ptr(cen, C.c_uint8), _ptr(st, C.c_int64),
-                                       cap, C.byref(n), C.byref(dropped)), self.h)
+                                       _ptr(lab, C.c_int32), cap, C.byref(n), C.byref(dropped)), self.h)
         k = n.value
         return (buf[: k * self.C].reshape(k, self.C), cen[: k * self.C].reshape(k, self.C).astype(bool),
-                st[:k].copy(), dropped.value)
+                st[:k].copy(), lab[:k].copy(), dropped.value)
+
+    # -- pH replica exchange -------------------------------------------------------------
+    def cph_exchange_energies(self, rows_dev_ptr):
+        _check(lib().cph_exchange_energies(self.h, C.c_void_p(int(rows_dev_ptr))), self.h)
+
+    def cph_exchange_apply(self, rows_all_dev_ptr, seed, attempt):
+        _check(lib().cph_exchange_apply(self.h, C.c_void_p(int(rows_all_dev_ptr)), int(seed), int(attempt)), self.h)
+
+    def cph_exchange(self, seed, attempt):
+        _check(lib().cph_exchange(self.h, int(seed), int(attempt)), self.h)
+
+    def exchange_device(self):
+        import torch
+        return torch.device("cuda", self.device)
+
+    def exchange_energies_into(self, t):
+        """Write this context's (label, E_p) rows into the float64 CUDA tensor t."""
+        import torch
+        assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and t.numel() >= self.R * (self.P + 1)
+        self.cph_exchange_energies(t.data_ptr())
+
+    def exchange_apply_from(self, t, seed, attempt):
+        import torch
+        assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+        self.cph_exchange_apply(t.data_ptr(), seed, attempt)
+
+    def cph_get_labels(self):
+        lab = np.zeros(self.R, np.int32)
+        _check(lib().cph_get_labels(self.h, _ptr(lab, C.c_int32)), self.h)
+        return lab
+
+    def cph_set_labels(self, labels):
+        lab = np.ascontiguousarray(labels, np.int32)
+        _check(lib().cph_set_labels(self.h, _ptr(lab, C.c_int32)), self.h)
+
+    def cph_get_exchange_stats(self, n_ladders):
+        n = n_ladders * (self.P - 1)
+        a = np.zeros(max(n, 1), np.int64)
+        b = np.zeros(max(n, 1), np.int64)
+        _check(lib().cph_get_exchange_stats(self.h, _ptr(a, C.c_int64), _ptr(b, C.c_int64)), self.h)
+        return a[:n].reshape(n_ladders, -1), b[:n].reshape(n_ladders, -1)
 
     def cph_get_dbo_params(self, r):
         """[C, 4]: (a0, a1, h_prot, h_deprot) per coordinate."""

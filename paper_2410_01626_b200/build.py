@@ -22,6 +22,7 @@ SOURCES = {
     "kernels_nb.cu": ["-ftz=true"],
     "kernels_pme.cu": ["-ftz=true"],
     "kernels_dyn.cu": ["-ftz=true"],
+    "kernels_remd.cu": [],
 }
 
 

@@ -176,6 +176,39 @@ __host__ __device__ inline void vmm_eval(const double *c, double lp, double lt, 
   *v = V; *dp = DP; *dt = DT;
 }
 
+// Bias of one lambda-group (Eq. 3) at (lp, lt): returns V and
+// dV/dlp, dV/dlt.  vmm36 == nullptr leaves Vmm out (the pH-independent term, e.g. for the
+// replica-exchange energies).  dG = (dG_macro, dG_delta, dG_eps) at the pH; d1 = PFC depths
+// of the group's coordinates; dw = DBO rows (a0, a1, h_prot, h_deprot) of its coordinates.
+__host__ __device__ inline double group_bias_eval(int kind, const double *vmm36, const double *dG, const double *d1,
+                                                  const double *dw, double kw, double lp, double lt, double *dp,
+                                                  double *dt) {
+  double vm = 0.0, vmp = 0.0, vmt = 0.0;
+  if (vmm36) vmm_eval(vmm36, lp, lt, &vm, &vmp, &vmt);
+  double vph, vphp, vpht;
+  if (kind == 2) { vph = lp * dG[0]; vphp = dG[0]; vpht = 0.0; }
+  else {
+    vph = lp * ((1.0 - lt) * dG[1] + lt * dG[2]);
+    vphp = (1.0 - lt) * dG[1] + lt * dG[2];
+    vpht = lp * (dG[2] - dG[1]);
+  }
+  double vd, vdp;
+  vdw_eval(lp, dw[0], dw[1], dw[2], d1[0], kw, &vd, &vdp, nullptr);
+  double V = vm + vph + vd;
+  *dt = 0.0;
+  if (kind == 3) {
+    const double *wt = dw + 4;
+    double ht, dht, vd2, vdt, vdh;
+    tautomer_barrier(lp, wt[2], wt[3], &ht, &dht);
+    vdw_eval(lt, wt[0], wt[1], ht, d1[1], kw, &vd2, &vdt, &vdh);
+    *dt = vmt + vpht + vdt;
+    vdp += vdh * dht;
+    V += vd2;
+  }
+  *dp = vmp + vphp + vdp;
+  return V;
+}
+
 __device__ inline double warp_sum_d(double v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;

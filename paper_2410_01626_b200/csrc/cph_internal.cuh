@@ -71,6 +71,8 @@ struct KParams {
   // Bussi thermostat (R27/R28): on/off, degrees of freedom, exp(-dt/tau)
   int bussi;
   double nf_atom, cb_atom, cb_lam;
+  // pH replica exchange (R29/R30): P levels (0 = off), global replica layout
+  int P, remd_total, remd_first;
 };
 
 struct DevBufs {
@@ -119,6 +121,14 @@ struct DevBufs {
   unsigned char *frame_cens = nullptr;              // [R*fcap*C]
   long long *frame_step = nullptr;                  // [R*fcap]
   double *bussi_k = nullptr;                        // [2*R] mid-step atom kinetic energy by step parity
+  // pH replica exchange
+  double *lvl_d1 = nullptr;                         // [P*C] PFC depths per pH level
+  double *lvl_dG = nullptr;                         // [P*G*3] dG per pH level
+  int *remd_label = nullptr;                        // [R] level index of each local replica
+  double *remd_rows = nullptr;                      // [R*(P+1)] (label, E_p) rows for cph_exchange
+  int *remd_holder = nullptr, *remd_newlab = nullptr;   // [remd_total] scratch of the apply kernel
+  long long *remd_att = nullptr, *remd_acc = nullptr;   // [L*(P-1)] attempts / accepts per pair
+  int *frame_label = nullptr;                       // [R*fcap]
 };
 
 struct DboConfig {
@@ -152,6 +162,8 @@ struct Ctx {
   std::vector<int> h_c_group, h_c_lp;               // [C]
   std::vector<long long> h_cens;                    // [R*G*2]
   std::vector<cph_dbo_event> events;                // undrained DBO log
+  std::vector<double> h_levels;                     // [P] pH ladder
+  std::vector<double> h_lvl_d1, h_lvl_dG;           // [P*C], [P*G*3]
   DboConfig dbo;
   int *h_flags_mapped = nullptr;                    // host view of a mapped flag copy
   int *d_flags_mapped = nullptr;
@@ -175,6 +187,9 @@ int launch_gather(Ctx &c, cudaStream_t s);
 int launch_lambda_reduce(Ctx &c, cudaStream_t s, int mode);       // 0 init eval, 1 step
 int launch_lambda_open(Ctx &c, cudaStream_t s);
 int launch_set_charges(Ctx &c, cudaStream_t s);
+int launch_remd_energy(Ctx &c, cudaStream_t s, double *rows);
+int launch_remd_apply(Ctx &c, cudaStream_t s, const double *rows_all, uint64_t seed, long long attempt);
+int launch_bias_refresh(Ctx &c, cudaStream_t s);
 
 // host PFC (pfc.cu); dw = (a0, a1, h_prot, h_deprot) of each coordinate of the site
 bool pfc_two_state(const double dw[4], double pKa, double pH, double T, double kw, double *d1, std::string *err);

@@ -110,12 +110,9 @@ bool finite_arr(const double *p, size_t n) {
 
 // PFC of replica r (all groups, or the groups flagged in `only`), with the current DBO
 // parameters of each coordinate: host arithmetic only, results in h_d1 / h_dG
-static bool compute_pfc(Ctx &c, int r, const std::vector<char> *only, std::string *err) {
+static bool compute_pfc_at(const Ctx &c, double pH, const double *dw, double *d1, double *dG,
+                           const std::vector<char> *only, std::string *err) {
   const KParams &kp = c.kp;
-  const double pH = c.h_pH[r];
-  double *dG = c.h_dG.data() + (size_t)r * kp.G * 3;
-  double *d1 = c.h_d1.data() + (size_t)r * kp.C;
-  const double *dw = c.h_dw.data() + (size_t)r * kp.C * 4;
   for (int g = 0; g < kp.G; ++g) {
     const double *pk = &c.h_pKa[(size_t)g * 3];
     for (int k = 0; k < 3; ++k) dG[(size_t)g * 3 + k] = delta_g(pk[k], pH, kp.kT / kBoltz);
@@ -130,32 +127,78 @@ static bool compute_pfc(Ctx &c, int r, const std::vector<char> *only, std::strin
   return true;
 }
 
+static bool compute_pfc(Ctx &c, int r, const std::vector<char> *only, std::string *err) {
+  const KParams &kp = c.kp;
+  return compute_pfc_at(c, c.h_pH[r], c.h_dw.data() + (size_t)r * kp.C * 4, c.h_d1.data() + (size_t)r * kp.C,
+                        c.h_dG.data() + (size_t)r * kp.G * 3, only, err);
+}
+
+// run f(k) for k in [0, n) on host threads
+template <class F>
+static void parallel_for(size_t n, F f) {
+  const size_t nt = std::max<size_t>(1, std::min<size_t>(n, std::thread::hardware_concurrency()));
+  std::atomic<size_t> next{0};
+  auto work = [&]() {
+    for (size_t k; (k = next.fetch_add(1)) < n;) f(k);
+  };
+  std::vector<std::thread> th;
+  for (size_t t = 1; t < nt; ++t) th.emplace_back(work);
+  work();
+  for (auto &t : th) t.join();
+}
+
 // PFC for a set of replicas (host threads, one replica per task), then one upload
 cph_status run_pfc_many(Ctx &c, const std::vector<int> &reps, const std::vector<std::vector<char>> *only = nullptr) {
   if (reps.empty()) return CPH_OK;
-  const int nt = (int)std::max<size_t>(1, std::min<size_t>(reps.size(), std::thread::hardware_concurrency()));
-  std::atomic<size_t> next{0};
   std::atomic<bool> failed{false};
   std::string ferr;
   std::mutex mu;
-  auto work = [&]() {
-    for (size_t k; (k = next.fetch_add(1)) < reps.size();) {
-      std::string e;
-      if (!compute_pfc(c, reps[k], only ? &(*only)[reps[k]] : nullptr, &e)) {
-        std::lock_guard<std::mutex> lk(mu);
-        failed = true;
-        ferr = e;
-      }
+  parallel_for(reps.size(), [&](size_t k) {
+    std::string e;
+    if (!compute_pfc(c, reps[k], only ? &(*only)[reps[k]] : nullptr, &e)) {
+      std::lock_guard<std::mutex> lk(mu);
+      failed = true;
+      ferr = e;
     }
-  };
-  std::vector<std::thread> th;
-  for (int t = 1; t < nt; ++t) th.emplace_back(work);
-  work();
-  for (auto &t : th) t.join();
+  });
   if (failed) { c.err = ferr; return CPH_E_INVALID; }
   const KParams &kp = c.kp;
   if (kp.C) CK(cudaMemcpy(c.d.d1, c.h_d1.data(), sizeof(double) * c.h_d1.size(), cudaMemcpyHostToDevice));
   if (kp.G) CK(cudaMemcpy(c.d.g_dG, c.h_dG.data(), sizeof(double) * c.h_dG.size(), cudaMemcpyHostToDevice));
+  return CPH_OK;
+}
+
+// pH ladder: PFC once per level (undisturbed wells), every replica takes its level's rows
+cph_status run_pfc_levels(Ctx &c, const std::vector<int> &labels) {
+  const KParams &kp = c.kp;
+  const int P = kp.P;
+  c.h_lvl_d1.assign((size_t)P * kp.C, 0.0);
+  c.h_lvl_dG.assign((size_t)P * kp.G * 3, 0.0);
+  std::vector<double> dw0((size_t)kp.C * 4);
+  for (int k = 0; k < kp.C; ++k) {
+    dw0[4 * k] = 0.0; dw0[4 * k + 1] = 1.0; dw0[4 * k + 2] = dw0[4 * k + 3] = kp.h_barrier;
+  }
+  std::atomic<bool> failed{false};
+  parallel_for(P, [&](size_t p) {
+    std::string e;
+    if (!compute_pfc_at(c, c.h_levels[p], dw0.data(), c.h_lvl_d1.data() + p * kp.C, c.h_lvl_dG.data() + p * kp.G * 3,
+                        nullptr, &e))
+      failed = true;
+  });
+  if (failed) { c.err = "PFC failed on the pH ladder"; return CPH_E_INVALID; }
+  for (int r = 0; r < kp.R; ++r) {
+    std::copy_n(c.h_lvl_d1.begin() + (size_t)labels[r] * kp.C, kp.C, c.h_d1.begin() + (size_t)r * kp.C);
+    std::copy_n(c.h_lvl_dG.begin() + (size_t)labels[r] * kp.G * 3, kp.G * 3, c.h_dG.begin() + (size_t)r * kp.G * 3);
+  }
+  if (kp.C) {
+    CK(cudaMemcpy(c.d.lvl_d1, c.h_lvl_d1.data(), sizeof(double) * c.h_lvl_d1.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c.d.d1, c.h_d1.data(), sizeof(double) * c.h_d1.size(), cudaMemcpyHostToDevice));
+  }
+  if (kp.G) {
+    CK(cudaMemcpy(c.d.lvl_dG, c.h_lvl_dG.data(), sizeof(double) * c.h_lvl_dG.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c.d.g_dG, c.h_dG.data(), sizeof(double) * c.h_dG.size(), cudaMemcpyHostToDevice));
+  }
+  CK(cudaMemcpy(c.d.remd_label, labels.data(), sizeof(int) * kp.R, cudaMemcpyHostToDevice));
   return CPH_OK;
 }
 
@@ -300,6 +343,10 @@ void cph_default_params(cph_params *p) {
   p->thermostat = 0;
   p->tau_atom = 0.1;
   p->tau_lambda = 1.0;
+  p->n_ph_levels = 0;
+  p->ph_levels = nullptr;
+  p->remd_first = 0;
+  p->remd_total = 0;
 }
 
 const char *cph_last_error(const cph_ctx *ctx) { return ctx ? ctx->c.err.c_str() : g_create_err.c_str(); }
@@ -347,6 +394,29 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   if (prm->thermostat != 0 && prm->thermostat != 1) return bad("thermostat must be 0 (Langevin) or 1 (Bussi)");
   if (prm->thermostat == 1 && !(prm->tau_atom > 0.0 && prm->tau_lambda > 0.0))
     return bad("Bussi coupling times must be > 0");
+  std::vector<int> labels0;
+  if (prm->n_ph_levels != 0) {
+    const int P = prm->n_ph_levels;
+    if (P < 2 || !prm->ph_levels || !finite_arr(prm->ph_levels, P)) return bad("replica exchange needs n_ph_levels >= 2 finite ph_levels");
+    for (int p = 1; p < P; ++p)
+      if (!(prm->ph_levels[p] > prm->ph_levels[p - 1])) return bad("ph_levels must be strictly ascending");
+    if (prm->mode != 0 || prm->dbo_well || prm->dbo_barrier) {
+      c.err = "pH replica exchange is not combinable with DBO or fixed-lambda mode";
+      return fail_create(ctx, CPH_E_UNSUPPORTED);
+    }
+    const int total = prm->remd_total ? prm->remd_total : R;
+    if (total % P || prm->remd_first < 0 || prm->remd_first + R > total)
+      return bad("remd_total must be a multiple of n_ph_levels and hold [remd_first, remd_first + R)");
+    if (!prm->pH) return bad("pH array is required");
+    for (int r = 0; r < R; ++r) {
+      int lab = -1;
+      for (int p = 0; p < P; ++p)
+        if (std::fabs(prm->pH[r] - prm->ph_levels[p]) <= 1e-9 * std::max(1.0, std::fabs(prm->ph_levels[p]))) lab = p;
+      if (lab < 0) return bad("every replica pH must be one of ph_levels");
+      labels0.push_back(lab);
+    }
+    c.h_levels.assign(prm->ph_levels, prm->ph_levels + P);
+  }
   if (prm->dbo_well || prm->dbo_barrier) {
     if ((prm->dbo_well && (prm->dbo_well_steps < 1 || prm->dbo_well_steps % prm->nstlist)) ||
         (prm->dbo_barrier && (prm->dbo_barrier_steps < 1 || prm->dbo_barrier_steps % prm->nstlist)) ||
@@ -504,6 +574,9 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     kp.dbo_on = on ? 1 : 0;
     kp.dbo_near = b.near; kp.dbo_trans_lo = b.trans_lo; kp.dbo_trans_hi = b.trans_hi;
   }
+  kp.P = prm->n_ph_levels;
+  kp.remd_total = kp.P ? (prm->remd_total ? prm->remd_total : R) : 0;
+  kp.remd_first = kp.P ? prm->remd_first : 0;
   kp.bussi = prm->thermostat == 1;
   {
     int mobile = 0;
@@ -586,6 +659,19 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   d.frame_cens = dalloc<unsigned char>(c, (size_t)R * kp.fcap * C);
   d.frame_step = dalloc<long long>(c, (size_t)R * kp.fcap);
   d.bussi_k = dalloc<double>(c, 2 * (size_t)R);
+  d.frame_label = dalloc<int>(c, (size_t)R * kp.fcap);
+  if (kp.P) {
+    const int P = kp.P, L = kp.remd_total / P;
+    d.lvl_d1 = dalloc<double>(c, (size_t)P * C);
+    d.lvl_dG = dalloc<double>(c, (size_t)P * G * 3);
+    d.remd_label = dalloc<int>(c, R);
+    d.remd_rows = dalloc<double>(c, (size_t)R * (P + 1));
+    d.remd_holder = dalloc<int>(c, kp.remd_total);
+    d.remd_newlab = dalloc<int>(c, kp.remd_total);
+    d.remd_att = dalloc<long long>(c, (size_t)L * (P - 1));
+    d.remd_acc = dalloc<long long>(c, (size_t)L * (P - 1));
+    if (!d.remd_acc) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
+  }
   for (void *p : {(void *)d.xyzq, (void *)d.nbl, (void *)d.grid, (void *)d.cgrid, (void *)d.flags, (void *)d.seed})
     if (!p) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
   if (c.allocations.size() < 40) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
@@ -668,7 +754,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   {
     std::vector<int> all(R);
     for (int r = 0; r < R; ++r) all[r] = r;
-    cph_status st = run_pfc_many(c, all);
+    cph_status st = kp.P ? run_pfc_levels(c, labels0) : run_pfc_many(c, all);
     if (st != CPH_OK) return fail_create(ctx, st);
   }
   // cuFFT plans (batched over replicas)
@@ -721,6 +807,7 @@ cph_status cph_set_pH(cph_ctx *ctx, int32_t replica, double pH) {
   cph_status st = check_replica(c, replica);
   if (st) return st;
   if (!std::isfinite(pH)) { c.err = "non-finite pH"; return CPH_E_INVALID; }
+  if (c.kp.P) { c.err = "pH is set through the replica-exchange labels (cph_set_labels)"; return CPH_E_STATE; }
   cudaSetDevice(c.device);
   CK(cudaStreamSynchronize(c.stream));
   const double old = c.h_pH[replica];
@@ -898,6 +985,11 @@ cph_status cph_get_bias_params(cph_ctx *ctx, int32_t r, double *d1) {
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
   if (st) return st;
+  if (d1 && c.kp.P) {          // labels may have moved on the device
+    if ((st = cph_sync(ctx))) return st;
+    if (c.kp.C) CK(cudaMemcpy(d1, c.d.d1 + (size_t)r * c.kp.C, sizeof(double) * c.kp.C, cudaMemcpyDeviceToHost));
+    return CPH_OK;
+  }
   if (d1) std::copy(c.h_d1.begin() + (size_t)r * c.kp.C, c.h_d1.begin() + (size_t)(r + 1) * c.kp.C, d1);
   return CPH_OK;
 }
@@ -915,8 +1007,8 @@ cph_status cph_get_energies(cph_ctx *ctx, int32_t r, double *e) {
   return CPH_OK;
 }
 
-cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t r, float *buf, uint8_t *censored, int64_t *steps, int64_t cap,
-                             int64_t *n_frames, int64_t *n_dropped) {
+cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t r, float *buf, uint8_t *censored, int64_t *steps, int32_t *labels,
+                             int64_t cap, int64_t *n_frames, int64_t *n_dropped) {
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
@@ -930,6 +1022,8 @@ cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t r, float *buf, uint8_t *censo
   std::vector<float> all((size_t)kp.fcap * kp.C);
   std::vector<unsigned char> cens((size_t)kp.fcap * kp.C);
   std::vector<long long> fst(kp.fcap);
+  std::vector<int> flab(kp.fcap);
+  CK(cudaMemcpy(flab.data(), c.d.frame_label + (size_t)r * kp.fcap, sizeof(int) * kp.fcap, cudaMemcpyDeviceToHost));
   if (kp.C) {
     CK(cudaMemcpy(all.data(), c.d.frames + (size_t)r * kp.fcap * kp.C, sizeof(float) * all.size(), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(cens.data(), c.d.frame_cens + (size_t)r * kp.fcap * kp.C, cens.size(), cudaMemcpyDeviceToHost));
@@ -944,6 +1038,7 @@ cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t r, float *buf, uint8_t *censo
       if (censored) censored[f * kp.C + k] = cens[(size_t)slot * kp.C + k];
     }
     if (steps) steps[f] = fst[slot];
+    if (labels) labels[f] = flab[slot];
   }
   if (n_frames) *n_frames = take;
   if (n_dropped) *n_dropped = total - take;
@@ -953,7 +1048,77 @@ cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t r, float *buf, uint8_t *censo
 }
 
 cph_status cph_get_frames(cph_ctx *ctx, int32_t r, float *buf, int64_t cap, int64_t *n_frames, int64_t *n_dropped) {
-  return cph_get_frames_ex(ctx, r, buf, nullptr, nullptr, cap, n_frames, n_dropped);
+  return cph_get_frames_ex(ctx, r, buf, nullptr, nullptr, nullptr, cap, n_frames, n_dropped);
+}
+
+static cph_status need_remd(Ctx &c) {
+  if (!c.kp.P) { c.err = "replica exchange is off (n_ph_levels = 0)"; return CPH_E_STATE; }
+  return CPH_OK;
+}
+
+cph_status cph_exchange_energies(cph_ctx *ctx, double *rows) {
+  if (!ctx || !rows) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  if (cph_status st = need_remd(c)) return st;
+  cudaSetDevice(c.device);
+  c.launches += launch_remd_energy(c, c.stream, rows);
+  CK(cudaGetLastError());
+  return CPH_OK;
+}
+
+cph_status cph_exchange_apply(cph_ctx *ctx, const double *rows_all, uint64_t seed, int64_t attempt) {
+  if (!ctx || !rows_all || attempt < 0) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  if (cph_status st = need_remd(c)) return st;
+  cudaSetDevice(c.device);
+  c.launches += launch_remd_apply(c, c.stream, rows_all, seed, attempt);
+  c.launches += launch_bias_refresh(c, c.stream);
+  CK(cudaGetLastError());
+  return CPH_OK;
+}
+
+cph_status cph_exchange(cph_ctx *ctx, uint64_t seed, int64_t attempt) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  if (cph_status st = need_remd(c)) return st;
+  if (c.kp.remd_total != c.kp.R) { c.err = "cph_exchange needs every replica in this context"; return CPH_E_STATE; }
+  cph_status st = cph_exchange_energies(ctx, c.d.remd_rows);
+  return st ? st : cph_exchange_apply(ctx, c.d.remd_rows, seed, attempt);
+}
+
+cph_status cph_get_labels(cph_ctx *ctx, int32_t *labels) {
+  if (!ctx || !labels) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = need_remd(c);
+  if (st || (st = cph_sync(ctx))) return st;
+  CK(cudaMemcpy(labels, c.d.remd_label, sizeof(int) * c.kp.R, cudaMemcpyDeviceToHost));
+  return CPH_OK;
+}
+
+cph_status cph_set_labels(cph_ctx *ctx, const int32_t *labels) {
+  if (!ctx || !labels) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = need_remd(c);
+  if (st) return st;
+  for (int r = 0; r < c.kp.R; ++r)
+    if (labels[r] < 0 || labels[r] >= c.kp.P) { c.err = "label out of range"; return CPH_E_INVALID; }
+  cudaSetDevice(c.device);
+  CK(cudaStreamSynchronize(c.stream));
+  std::vector<int> lab(labels, labels + c.kp.R);
+  if ((st = run_pfc_levels(c, lab))) return st;
+  c.launches += launch_bias_refresh(c, c.stream);
+  return check_flags(c);
+}
+
+cph_status cph_get_exchange_stats(cph_ctx *ctx, int64_t *attempts, int64_t *accepts) {
+  if (!ctx) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = need_remd(c);
+  if (st || (st = cph_sync(ctx))) return st;
+  const size_t n = (size_t)(c.kp.remd_total / c.kp.P) * (c.kp.P - 1);
+  if (attempts) CK(cudaMemcpy(attempts, c.d.remd_att, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+  if (accepts) CK(cudaMemcpy(accepts, c.d.remd_acc, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+  return CPH_OK;
 }
 
 cph_status cph_get_dbo_params(cph_ctx *ctx, int32_t r, double *p) {

@@ -234,34 +234,16 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
       sp += s_dq[2 * k];
       st += s_dq[2 * k + 1];
     }
-    // bias (Eq. 3): Vmm + VpH + Vdw
-    double vm, vmp, vmt;
-    vmm_eval(d.vmm + 36 * (size_t)g, lp, lt, &vm, &vmp, &vmt);
-    const double *dG = d.g_dG + ((size_t)r * kp.G + g) * 3;
-    double vph, vphp, vpht;
-    if (kind == 2) { vph = lp * dG[0]; vphp = dG[0]; vpht = 0.0; }
-    else {
-      vph = lp * ((1.0 - lt) * dG[1] + lt * dG[2]);
-      vphp = (1.0 - lt) * dG[1] + lt * dG[2];
-      vpht = lp * (dG[2] - dG[1]);
-    }
-    // double wells with the DBO parameters (a0, a1, h_prot, h_deprot) of each coordinate
-    const double *wp = d.dw + ic * 4;
-    double vd, vdp;
-    vdw_eval(lp, wp[0], wp[1], wp[2], d.d1[ic], kp.wall_k, &vd, &vdp, nullptr);
+    // bias (Eq. 3): Vmm + VpH + Vdw, double wells with the DBO parameters of each coordinate
+    double bp, bt;
+    ebias += group_bias_eval(kind, d.vmm + 36 * (size_t)g, d.g_dG + ((size_t)r * kp.G + g) * 3, d.d1 + ic,
+                             d.dw + ic * 4, kp.wall_k, lp, lt, &bp, &bt);
     d.dvdl_coul[ic] = f * sp;
-    ebias += vm + vph + vd;
+    d.dvdl_bias[ic] = bp;
     if (kind == 3) {
-      const double *wt = wp + 4;
-      double ht, dht, vd2, vdt, vdh;
-      tautomer_barrier(lp, wt[2], wt[3], &ht, &dht);
-      vdw_eval(lt, wt[0], wt[1], ht, d.d1[ic + 1], kp.wall_k, &vd2, &vdt, &vdh);
       d.dvdl_coul[ic + 1] = f * st;
-      d.dvdl_bias[ic + 1] = vmt + vpht + vdt;
-      vdp += vdh * dht;
-      ebias += vd2;
+      d.dvdl_bias[ic + 1] = bt;
     }
-    d.dvdl_bias[ic] = vmp + vphp + vdp;
   }
   ebias = block_sum_d(ebias);   // includes __syncthreads: dV/dlambda visible to the block
   // closing half kick, frames, TI accumulation, divergence
@@ -304,6 +286,7 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
   if (threadIdx.x == 0) {
     if (frame) {
       d.frame_step[(size_t)r * kp.fcap + fslot] = m;
+      d.frame_label[(size_t)r * kp.fcap + fslot] = kp.P ? d.remd_label[r] : -1;
       d.frame_total[r] += 1;
     }
     if (energy) {

@@ -89,7 +89,7 @@ def test_dbo_short_run_events_censor_and_trajectory_match_oracle(cph):
     np.testing.assert_allclose(ctx.cph_get_dbo_params(0), ref.dbo_params, atol=1e-5)
     np.testing.assert_allclose(ctx.cph_get_bias_params(0), ref.d1, atol=1e-4)
     # frames: steps 0..60 (nstout 1), censor flags per the oracle's rule on the site's events
-    fr, cens, steps, dropped = ctx.cph_get_frames_ex(0)
+    fr, cens, steps, _, dropped = ctx.cph_get_frames_ex(0)
     assert dropped == 0 and np.array_equal(steps, np.arange(61))
     group_of = np.array([0, 1, 1])
     for c in range(3):
@@ -140,7 +140,7 @@ def test_dbo_regulates_transitions_and_keeps_populations(cph):
     for k in range(len(levels)):
         x = []
         for r in range(k * per, (k + 1) * per):
-            fr, cens, steps, dropped = ctx.cph_get_frames_ex(r)
+            fr, cens, steps, _, dropped = ctx.cph_get_frames_ex(r)
             assert dropped == 0
             prm = ctx.cph_get_dbo_params(r)
             assert np.all(np.abs(prm[:, 0]) <= 0.08 + 1e-12) and np.all(np.abs(prm[:, 1] - 1) <= 0.08 + 1e-12)
