@@ -19,6 +19,19 @@ def deprotonated_fraction(lp_frames):
     return float(np.mean(lp >= 0.5))
 
 
+def micro_fractions(lp_frames, lt_frames):
+    """His microscopic ratios: x_delta = N_{deprot, t=0} / (N_prot +
+    N_{deprot, t=0}), x_eps = N_{deprot, t=1} / (N_prot + N_{deprot, t=1}); deprotonated iff
+    lambda_p >= 0.5 (R1), tautomer t = 0 (delta) iff lambda_t < 0.5 (R4)."""
+    lp = np.asarray(lp_frames, np.float64)
+    lt = np.asarray(lt_frames, np.float64)
+    deprot = lp >= 0.5
+    n_prot = np.count_nonzero(~deprot)
+    n_d = np.count_nonzero(deprot & (lt < 0.5))
+    n_e = np.count_nonzero(deprot & (lt >= 0.5))
+    return n_d / (n_prot + n_d), n_e / (n_prot + n_e)
+
+
 def hh(pH, pKa, n=1.0):
     return 1.0 / (10.0 ** (n * (pKa - np.asarray(pH, np.float64))) + 1.0)
 

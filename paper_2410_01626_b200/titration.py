@@ -56,6 +56,24 @@ def deprotonated_fraction(lambda_p_frames, censored=None) -> float:
     return float(np.count_nonzero(lp >= 0.5)) / lp.size
 
 
+def micro_fractions(lambda_p_frames, lambda_t_frames, censored=None):
+    """His microscopic deprotonation ratios, each fitted with the H-H
+    curve to give pKa_delta and pKa_eps: x_delta = N(deprot, lambda_t < 0.5) / (N_prot +
+    N(deprot, lambda_t < 0.5)) and x_eps likewise with lambda_t >= 0.5."""
+    lp = np.asarray(lambda_p_frames, np.float64)
+    lt = np.asarray(lambda_t_frames, np.float64)
+    if censored is not None:
+        keep = ~np.asarray(censored, bool)
+        lp, lt = lp[keep], lt[keep]
+    if lp.size == 0 or lp.shape != lt.shape:
+        raise ValueError("need matching, non-empty lambda_p / lambda_t frames")
+    deprot = lp >= 0.5
+    n_prot = np.count_nonzero(~deprot)
+    n_d = np.count_nonzero(deprot & (lt < 0.5))
+    n_e = np.count_nonzero(deprot & (lt >= 0.5))
+    return n_d / max(n_prot + n_d, 1), n_e / max(n_prot + n_e, 1)
+
+
 def _model(pH, pKa, n):
     return 1.0 / (np.power(10.0, n * (pKa - pH)) + 1.0)
 

@@ -86,3 +86,23 @@ def test_fit_vmm_matches_oracle_fit():
     g1 = g[:14, :1]
     x = np.array(T.TI_GRID)
     np.testing.assert_allclose(T.fit_vmm(2, x, None, g1), vmm_from_ti(2, x, None, g1), atol=1e-9)
+
+
+def test_his_micro_pka_recovered_from_exact_populations():
+    """3-state His populations at Table 2 micro pKa values (6.53, 6.92):
+    the micro ratios of PAPER.md:982-983 are H-H curves in the micro pKa, so fitting them
+    returns the inputs (closed form); the library's counting matches the oracle's."""
+    pk_d, pk_e = 6.53, 6.92
+    levels = np.linspace(5.5, 8.0, 6)
+    xd, xe = [], []
+    for pH in levels:
+        w = np.array([1.0, 10 ** (pH - pk_d), 10 ** (pH - pk_e)])
+        n = np.round(w / w.sum() * 200000).astype(int)
+        lp = np.concatenate([np.zeros(n[0]), np.ones(n[1] + n[2])])
+        lt = np.concatenate([np.full(n[0], 0.3), np.zeros(n[1]), np.ones(n[2])])
+        a, b = T.micro_fractions(lp, lt)
+        assert (a, b) == OA.micro_fractions(lp, lt)
+        xd.append(a)
+        xe.append(b)
+    assert abs(T.fit_curve(levels, np.array(xd)) - pk_d) < 1e-3
+    assert abs(T.fit_curve(levels, np.array(xe)) - pk_e) < 1e-3
