@@ -12,6 +12,9 @@ Follows, in order:
     With params thermostat="bussi" the O step is the Bussi velocity rescaling of the
     group (atoms tau_atom = 0.1 ps, lambda tau_lambda = 1 ps; PAPER.md:888, :902-906;
     oracle.thermostat, readings R27/R28).
+  * Optional Hamiltonian interpolation (params hamiltonian=True; oracle.hamiltonian,
+    PAPER.md:597-600): E_coul + sum_g C_g, its lambda derivative added to dvdl_coul and its
+    forces to F (energy term "hi").
     Atoms: m from the system, mass 0 = frozen.  lambda: m = 60 u,
     gamma = 1/tau = 1 ps^-1.  Noise from oracle.philox.
   * Partition Function Correction at construction.
@@ -28,6 +31,7 @@ from . import bias as B
 from . import dbo as DBO
 from . import pfc as PFC
 from . import thermostat as TH
+from . import hamiltonian as HI
 from .charges import charges, coord_ptr
 from .ewald import (ewald_beta, exclusion_correction, net_charge_term, real_space,
                     recip_direct, self_term)
@@ -35,7 +39,7 @@ from .philox import normals
 from .pme import pme
 from .units import F_COUL, kT
 
-ENERGY_TERMS = ("LJ", "real", "excl", "self", "recip", "net", "bias", "KE_atoms", "KE_lambda", "total")
+ENERGY_TERMS = ("LJ", "real", "excl", "self", "recip", "net", "hi", "bias", "KE_atoms", "KE_lambda", "total")
 
 
 class OracleReplica:
@@ -172,9 +176,17 @@ class OracleReplica:
                     dvdl_coul[c0 + 1] += F_COUL * dq[k, 1] * phi[i]
                     term_mag[c0 + 1] += abs(F_COUL * dq[k, 1] * phi[i])
         e_bias, dvdl_bias = self.bias(lam)
+        e_hi = 0.0
+        if p.get("hamiltonian", False):
+            if getattr(self, "_kv", None) is None:
+                self._kv = HI.kvectors(self.box, self.beta)
+            e_hi, dv_hi, f_hi = HI.hi_terms(s, x, lam, self.cptr, self.box, self.beta, p["rc"], self._kv)
+            dvdl_coul = dvdl_coul + dv_hi
+            term_mag = term_mag + np.abs(dv_hi)
+            F = F + f_hi
         return dict(q=q, phi=phi, F=F, dvdl_coul=dvdl_coul, dvdl_bias=dvdl_bias, term_mag=term_mag,
                     E=dict(LJ=rs["E_LJ"], real=rs["E_real"], excl=ex["E_excl"], self=e_self,
-                           recip=e_rec, net=e_net, bias=e_bias),
+                           recip=e_rec, net=e_net, hi=e_hi, bias=e_bias),
                     phi_parts=dict(real=rs["phi"], excl=ex["phi"], recip=phi_rec, self=phi_self, net=phi_net))
 
     def energies(self):

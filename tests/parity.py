@@ -3,7 +3,7 @@ import numpy as np
 
 RTOL = 2e-5        # potentials, forces, dV/dlambda (north star)
 ETOL = 1e-6        # total energy (north star)
-POT_TERMS = ("LJ", "real", "excl", "self", "recip", "net", "bias")
+POT_TERMS = ("LJ", "real", "excl", "self", "recip", "net", "hi", "bias")
 
 
 def force_err(f_gpu, f_ref):
