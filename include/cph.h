@@ -16,6 +16,8 @@
  *   a9  BAOAB Langevin / velocity-Verlet update of atoms and lambda particles
  *       (m_lambda = 60 u), dt = 2 fs, 300 K;
  *   f2  or, instead of the Langevin O step, the paper's Bussi thermostat.
+ *   f3  pH replica exchange across replicas / GPUs (cph_exchange*).
+ *   f4  optional Hamiltonian interpolation (params.hamiltonian).
  *   a10 Partition Function Correction of the double-well depths at cph_create /
  *       cph_set_pH.
  *   f1  optional Dynamic Barrier and Well Optimization with censoring
@@ -72,13 +74,14 @@ typedef enum {
 /* energy terms returned by cph_get_energies, kJ/mol */
 enum {
   CPH_E_LJ = 0, CPH_E_REAL, CPH_E_EXCL, CPH_E_SELF, CPH_E_RECIP, CPH_E_NET,
+  CPH_E_HI,      /* Hamiltonian-interpolation correction sum_g C_g (0 unless params.hamiltonian) */
   CPH_E_BIAS, CPH_E_KE_ATOMS, CPH_E_KE_LAMBDA, CPH_E_TOTAL, CPH_N_ETERMS
 };
 
 /* kernel classes timed by cph_profile_steps */
 enum {
   CPH_K_INTEGRATE = 0, CPH_K_PAIRLIST, CPH_K_NONBONDED, CPH_K_SPREAD, CPH_K_FFT_R2C,
-  CPH_K_SOLVE, CPH_K_FFT_C2R, CPH_K_GATHER, CPH_K_LAMBDA, CPH_N_KCLASSES
+  CPH_K_SOLVE, CPH_K_FFT_C2R, CPH_K_GATHER, CPH_K_LAMBDA, CPH_K_HI, CPH_N_KCLASSES
 };
 
 typedef struct {
@@ -174,6 +177,13 @@ typedef struct {
   const double *ph_levels;      /* [P] strictly ascending pH levels */
   int32_t remd_first;           /* global index of this context's replica 0 (0) */
   int32_t remd_total;           /* replicas over all contexts, multiple of P (0 = R) */
+  /* 0: charge interpolation (default, the north star's PME scheme); 1: Hamiltonian
+   * interpolation, Eq. 1 literally (R31): E_coul of
+   * the interpolated charges plus, per lambda-group, C = 1/4 sum_{s,t} w_s w_t D_st with
+   * D_st = (q^s - q^t)^T G (q^s - q^t) over the group's atoms (real space, exclusion, self
+   * and exact Ewald reciprocal terms); its lambda derivative is part of the Coulomb
+   * dV/dlambda and its forces of the atom forces.  Groups of at most 32 atoms. */
+  int32_t hamiltonian;
 } cph_params;
 
 /* DBO event kinds (cph_dbo_event.kind) */

@@ -21,9 +21,9 @@ LIB_PATH = os.path.join(_HERE, "libcph.so")
 CPH_ABI_VERSION = 2
 STATUS = {0: "CPH_OK", 1: "CPH_E_INVALID", 2: "CPH_E_CUDA", 3: "CPH_E_DIVERGED", 4: "CPH_E_STATE",
           5: "CPH_E_OOM", 6: "CPH_E_UNSUPPORTED"}
-ENERGY_TERMS = ("LJ", "real", "excl", "self", "recip", "net", "bias", "KE_atoms", "KE_lambda", "total")
+ENERGY_TERMS = ("LJ", "real", "excl", "self", "recip", "net", "hi", "bias", "KE_atoms", "KE_lambda", "total")
 KERNEL_CLASSES = ("integrate", "pairlist", "nonbonded", "spread", "fft_r2c", "solve", "fft_c2r",
-                  "gather", "lambda")
+                  "gather", "lambda", "hi")
 N_ETERMS = len(ENERGY_TERMS)
 
 _p = C.POINTER
@@ -58,7 +58,7 @@ class cph_params(C.Structure):
                 ("dbo_barrier_min", C.c_double), ("dbo_barrier_max", C.c_double),
                 ("thermostat", C.c_int32), ("tau_atom", C.c_double), ("tau_lambda", C.c_double),
                 ("n_ph_levels", C.c_int32), ("ph_levels", _f64p), ("remd_first", C.c_int32),
-                ("remd_total", C.c_int32)]
+                ("remd_total", C.c_int32), ("hamiltonian", C.c_int32)]
 
 
 class cph_dbo_event(C.Structure):
@@ -221,7 +221,7 @@ def cph_create(system, pH, replica_seed, *, lambda0=None, pos_replicas=None, vel
         if k in params:
             setattr(p, k, float(params[k]))
     for k in ("pme_order", "nstlist", "nstout", "nstenergy", "frame_capacity", "dbo_well", "dbo_barrier",
-              "dbo_well_steps", "dbo_barrier_steps", "dbo_censor_steps"):
+              "dbo_well_steps", "dbo_barrier_steps", "dbo_censor_steps", "hamiltonian"):
         if k in params:
             setattr(p, k, int(params[k]))
     if "thermostat" in params:

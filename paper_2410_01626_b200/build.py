@@ -23,6 +23,7 @@ SOURCES = {
     "kernels_pme.cu": ["-ftz=true"],
     "kernels_dyn.cu": ["-ftz=true"],
     "kernels_remd.cu": [],
+    "kernels_hi.cu": [],
 }
 
 

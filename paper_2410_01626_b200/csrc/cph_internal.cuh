@@ -73,6 +73,8 @@ struct KParams {
   double nf_atom, cb_atom, cb_lam;
   // pH replica exchange (R29/R30): P levels (0 = off), global replica layout
   int P, remd_total, remd_first;
+  // Hamiltonian interpolation (R31): on/off, reciprocal m-list size, table extents
+  int hi, hi_nm, hi_kmax[3], hi_nsplit;
 };
 
 struct DevBufs {
@@ -129,6 +131,13 @@ struct DevBufs {
   int *remd_holder = nullptr, *remd_newlab = nullptr;   // [remd_total] scratch of the apply kernel
   long long *remd_att = nullptr, *remd_acc = nullptr;   // [L*(P-1)] attempts / accepts per pair
   int *frame_label = nullptr;                       // [R*fcap]
+  // Hamiltonian interpolation
+  int4 *hi_m = nullptr;                             // [hi_nm] half-space m (integers)
+  float *hi_w = nullptr;                            // [hi_nm] 2 exp(-pi^2 m^2/beta^2)/(pi V m^2)
+  uint32_t *hi_excl = nullptr;                      // [nlam] intra-group exclusion mask per atom
+  double *hi_M = nullptr;                           // [R*G*10] reciprocal form matrix (without f)
+  float *hi_F = nullptr;                            // [R*nlam*3] reciprocal force sums (without 4 pi f)
+  double *hi_dvdl = nullptr;                        // [R*C] dC/dlambda
 };
 
 struct DboConfig {
@@ -190,6 +199,8 @@ int launch_set_charges(Ctx &c, cudaStream_t s);
 int launch_remd_energy(Ctx &c, cudaStream_t s, double *rows);
 int launch_remd_apply(Ctx &c, cudaStream_t s, const double *rows_all, uint64_t seed, long long attempt);
 int launch_bias_refresh(Ctx &c, cudaStream_t s);
+int launch_hi_recip(Ctx &c, cudaStream_t s);
+int launch_hi_finish(Ctx &c, cudaStream_t s, int step_offset);
 
 // host PFC (pfc.cu); dw = (a0, a1, h_prot, h_deprot) of each coordinate of the site
 bool pfc_two_state(const double dw[4], double pKa, double pH, double T, double kw, double *d1, std::string *err);

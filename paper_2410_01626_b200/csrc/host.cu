@@ -225,11 +225,13 @@ int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
   k += launch_solve(c, sp, 1);
   cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid);
   k += launch_gather(c, sp);
+  k += launch_hi_recip(c, sp);
   k += launch_nonbonded(c, s, 1);
   if (two_streams) {
     cudaEventRecord(c.ev_join, c.stream_pme);
     cudaStreamWaitEvent(s, c.ev_join, 0);
   }
+  k += launch_hi_finish(c, s, 1);
   k += launch_lambda_reduce(c, s, 1);
   return k;
 }
@@ -251,6 +253,8 @@ cph_status evaluate_here(Ctx &c) {
   CKF(cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid));
   k += launch_gather(c, s);
   k += launch_nonbonded(c, s, 0);
+  k += launch_hi_recip(c, s);
+  k += launch_hi_finish(c, s, 0);
   k += launch_lambda_reduce(c, s, 0);
   k += launch_close(c, s, 0);
   c.launches += k;
@@ -347,6 +351,7 @@ void cph_default_params(cph_params *p) {
   p->ph_levels = nullptr;
   p->remd_first = 0;
   p->remd_total = 0;
+  p->hamiltonian = 0;
 }
 
 const char *cph_last_error(const cph_ctx *ctx) { return ctx ? ctx->c.err.c_str() : g_create_err.c_str(); }
@@ -392,6 +397,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     return bad("nstlist, nstout, nstenergy, frame_capacity must be >= 1");
   if (prm->mode != 0 && prm->mode != 1) return bad("mode must be 0 or 1");
   if (prm->thermostat != 0 && prm->thermostat != 1) return bad("thermostat must be 0 (Langevin) or 1 (Bussi)");
+  if (prm->hamiltonian != 0 && prm->hamiltonian != 1) return bad("hamiltonian must be 0 or 1");
   if (prm->thermostat == 1 && !(prm->tau_atom > 0.0 && prm->tau_lambda > 0.0))
     return bad("Bussi coupling times must be > 0");
   std::vector<int> labels0;
@@ -495,6 +501,12 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     c.h_pKa.assign(sys->pKa, sys->pKa + 3 * (size_t)G);
   }
   const int C = c.h_cptr[G];
+  if (prm->hamiltonian)
+    for (int g = 0; g < G; ++g)
+      if (c.h_group_ptr[g + 1] - c.h_group_ptr[g] > 32) {
+        c.err = "Hamiltonian interpolation supports lambda-groups of at most 32 atoms";
+        return fail_create(ctx, CPH_E_UNSUPPORTED);
+      }
   if (nlam > 12000) { c.err = "more than 12000 lambda atoms per replica"; return fail_create(ctx, CPH_E_UNSUPPORTED); }
   if (prm->lambda0 && !finite_arr(prm->lambda0, (size_t)R * C)) return bad("non-finite lambda0");
 
@@ -577,6 +589,27 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   kp.P = prm->n_ph_levels;
   kp.remd_total = kp.P ? (prm->remd_total ? prm->remd_total : R) : 0;
   kp.remd_first = kp.P ? prm->remd_first : 0;
+  kp.hi = prm->hamiltonian == 1 && G > 0;
+  std::vector<int4> hi_m;
+  std::vector<float> hi_w;
+  if (kp.hi) {
+    // half-space m with exp(-pi^2 m^2/beta^2) >= 1e-8 (R31), 2 g(m) weights
+    const double mmax2 = -std::log(1e-8) * kp.beta_d * kp.beta_d / (kPi * kPi);
+    for (int e = 0; e < 3; ++e) kp.hi_kmax[e] = (int)std::floor(std::sqrt(mmax2) * sys->box[e]);
+    for (int nz = 0; nz <= kp.hi_kmax[2]; ++nz)
+      for (int ny = -kp.hi_kmax[1]; ny <= kp.hi_kmax[1]; ++ny)
+        for (int nx = -kp.hi_kmax[0]; nx <= kp.hi_kmax[0]; ++nx) {
+          if (nz == 0 && (ny < 0 || (ny == 0 && nx <= 0))) continue;
+          const double mx = nx / sys->box[0], my = ny / sys->box[1], mz = nz / sys->box[2];
+          const double m2 = mx * mx + my * my + mz * mz;
+          if (m2 > mmax2) continue;
+          hi_m.push_back(make_int4(nx, ny, nz, 0));
+          hi_w.push_back((float)(2.0 * std::exp(-kPi * kPi * m2 / (kp.beta_d * kp.beta_d)) / (kPi * V * m2)));
+        }
+    kp.hi_nm = (int)hi_m.size();
+    const int want = (2 * 148 + G * R - 1) / (G * R);
+    kp.hi_nsplit = std::max(1, std::min((kp.hi_nm + 255) / 256, want));
+  }
   kp.bussi = prm->thermostat == 1;
   {
     int mobile = 0;
@@ -660,6 +693,15 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   d.frame_step = dalloc<long long>(c, (size_t)R * kp.fcap);
   d.bussi_k = dalloc<double>(c, 2 * (size_t)R);
   d.frame_label = dalloc<int>(c, (size_t)R * kp.fcap);
+  if (kp.hi) {
+    d.hi_m = dalloc<int4>(c, kp.hi_nm);
+    d.hi_w = dalloc<float>(c, kp.hi_nm);
+    d.hi_excl = dalloc<uint32_t>(c, nlam);
+    d.hi_M = dalloc<double>(c, (size_t)R * G * 10);
+    d.hi_F = dalloc<float>(c, (size_t)R * nlam * 3);
+    d.hi_dvdl = dalloc<double>(c, (size_t)R * C);
+    if (!d.hi_dvdl) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
+  }
   if (kp.P) {
     const int P = kp.P, L = kp.remd_total / P;
     d.lvl_d1 = dalloc<double>(c, (size_t)P * C);
@@ -737,6 +779,21 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
         for (int g = 0; g < G; ++g)
           for (int k = c.h_group_ptr[g]; k < c.h_group_ptr[g + 1]; ++k) kg[k] = g;
         UP(d.k_group, kg.data(), nlam);
+      }
+      if (kp.hi) {
+        UP(d.hi_m, hi_m.data(), hi_m.size());
+        UP(d.hi_w, hi_w.data(), hi_w.size());
+        std::vector<uint32_t> mask(nlam, 0u);
+        for (int g = 0; g < G; ++g)
+          for (int i = c.h_group_ptr[g]; i < c.h_group_ptr[g + 1]; ++i) {
+            const int a = c.h_group_atoms[i];
+            for (int j = c.h_group_ptr[g]; j < c.h_group_ptr[g + 1]; ++j) {
+              const int b = c.h_group_atoms[j];
+              for (int e = c.h_excl_ptr[a]; e < c.h_excl_ptr[a + 1]; ++e)
+                if (c.h_excl_idx[e] == b) mask[i] |= 1u << (j - c.h_group_ptr[g]);
+            }
+          }
+        UP(d.hi_excl, mask.data(), nlam);
       }
       if (C) {
         UP(d.lam, lam0.data(), (size_t)R * C);
@@ -1400,7 +1457,7 @@ cph_status cph_profile_steps(cph_ctx *ctx, int64_t n_steps, double *ms, int64_t 
   cufftSetStream(c.plan_c2r, s);
   while (c.host_step < end) {
     const bool rebuild = (c.host_step + 1) % c.kp.nstlist == 0;
-    k += launch_integrate(c, s, 1); cnt[CPH_K_INTEGRATE] += 1; mark(CPH_K_INTEGRATE);
+    { int q = launch_integrate(c, s, 1); k += q; cnt[CPH_K_INTEGRATE] += q; mark(CPH_K_INTEGRATE); }
     if (rebuild) { int q = launch_rebuild(c, s); k += q; cnt[CPH_K_PAIRLIST] += q; mark(CPH_K_PAIRLIST); }
     k += launch_nonbonded(c, s, 1); cnt[CPH_K_NONBONDED] += 1; mark(CPH_K_NONBONDED);
     k += launch_spread(c, s); cnt[CPH_K_SPREAD] += 1; mark(CPH_K_SPREAD);
@@ -1408,6 +1465,10 @@ cph_status cph_profile_steps(cph_ctx *ctx, int64_t n_steps, double *ms, int64_t 
     k += launch_solve(c, s, 1); cnt[CPH_K_SOLVE] += 1; mark(CPH_K_SOLVE);
     cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid); mark(CPH_K_FFT_C2R);
     k += launch_gather(c, s); cnt[CPH_K_GATHER] += 1; mark(CPH_K_GATHER);
+    if (c.kp.hi) {
+      int q = launch_hi_recip(c, s) + launch_hi_finish(c, s, 1);
+      k += q; cnt[CPH_K_HI] += q; mark(CPH_K_HI);
+    }
     k += launch_lambda_reduce(c, s, 1); cnt[CPH_K_LAMBDA] += 1; mark(CPH_K_LAMBDA);
     c.host_step += 1;
   }

@@ -238,10 +238,11 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
     double bp, bt;
     ebias += group_bias_eval(kind, d.vmm + 36 * (size_t)g, d.g_dG + ((size_t)r * kp.G + g) * 3, d.d1 + ic,
                              d.dw + ic * 4, kp.wall_k, lp, lt, &bp, &bt);
-    d.dvdl_coul[ic] = f * sp;
+    // Hamiltonian interpolation: + dC/dlambda of the group (kernels_hi.cu)
+    d.dvdl_coul[ic] = f * sp + (kp.hi ? d.hi_dvdl[ic] : 0.0);
     d.dvdl_bias[ic] = bp;
     if (kind == 3) {
-      d.dvdl_coul[ic + 1] = f * st;
+      d.dvdl_coul[ic + 1] = f * st + (kp.hi ? d.hi_dvdl[ic + 1] : 0.0);
       d.dvdl_bias[ic + 1] = bt;
     }
   }
