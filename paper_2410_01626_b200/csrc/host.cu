@@ -1307,7 +1307,7 @@ cph_status cph_get_pairlist(cph_ctx *ctx, int32_t r, int32_t *pairs, int64_t cap
   for (size_t i = 0; i < N; ++i) {
     const int oi = meta[i].x;
     for (int k = 0; k < std::min(nnb[i], kp.cap); ++k) {
-      const int j = (int)(nbl[(size_t)k * kp.Nst + i] & kEntryJMask);
+      const int j = (int)(nbl[((size_t)(k / 8) * kp.Nst + i) * 8 + (k % 8)] & kEntryJMask);
       const int oj = meta[j].x;
       if (oi < oj) out.emplace_back(oi, oj);
     }

@@ -6,8 +6,9 @@
 // permuted.  Then each atom gets a FULL neighbour list (both directions, so the pair kernel
 // needs no atomics) of the non-excluded atoms with float32 d^2 < rlist^2, evaluated with the
 // canonical round-to-nearest, no-contraction formula of DESIGN.md R14 so that the list is
-// bit-exact against the oracle's.  Entries: sorted slot (24 bits) | LJ type (8 bits); stored
-// k-major (nbl[k][i]) so a warp reads 128 contiguous bytes per neighbour index.
+// bit-exact against the oracle's.  Entries: sorted slot (21 bits) | LJ type (5 bits) | image
+// code (5 bits); stored in 8-entry tiles nbl[k/8][i][k%8] so the builder writes whole 32-byte
+// sectors per lane and a warp of the pair kernel reads 1 KB contiguous per 8 neighbours.
 #include "cph_device.cuh"
 
 namespace cph {
@@ -172,6 +173,7 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
   const int *start = d.cell_start + (size_t)r * (kp.ncell + 1);
   __shared__ float4 sx[32];
   __shared__ int sj[32];
+  __shared__ uint32_t s_buf[16][32];
   const int cz = c % kp.nc[2], cy = (c / kp.nc[2]) % kp.nc[1], cx = c / (kp.nc[2] * kp.nc[1]);
   const int ib = start[c], ie = start[c + 1];
   const float3 Lbox = make_float3(kp.L[0], kp.L[1], kp.L[2]);
@@ -201,28 +203,57 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
     }
   }
   __syncwarp();
+  // [start, end) of every stencil cell, in the walk order (ox, oy, oz)
+  __shared__ int s_jb[125], s_je[125];
+  {
+    const int nyz = kp.ns[1] * kp.ns[2], nst = kp.ns[0] * nyz;
+    for (int t = lane; t < nst; t += 32) {
+      const int ox = t / nyz, oy = (t / kp.ns[2]) % kp.ns[1], oz = t % kp.ns[2];
+      const int cc = (s_cell[0][ox] * kp.nc[1] + s_cell[1][oy]) * kp.nc[2] + s_cell[2][oz];
+      s_jb[t] = start[cc];
+      s_je[t] = start[cc + 1];
+    }
+  }
+  __syncwarp();
   for (int i0 = ib; i0 < ie; i0 += 32) {
     const int i = i0 + lane;
     const bool valid = i < ie;
     const float4 xi = valid ? xq[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     const int orig = valid ? meta[i].x : 0;
     const int eb = valid ? d.excl_ptr[orig] : 0, ee = valid ? d.excl_ptr[orig + 1] : 0;
-    uint32_t *out = d.nbl + (size_t)r * kp.cap * kp.Nst + (valid ? i : 0);
-    const size_t ostride = kp.Nst;
-    int cnt = 0;
-    for (int ox = 0; ox < kp.ns[0]; ++ox) {
-      const int gx = s_cell[0][ox];
-      const float wsx = s_wsh[0][ox];
-      for (int oy = 0; oy < kp.ns[1]; ++oy) {
-        const int gy = s_cell[1][oy];
-        const float wsy = s_wsh[1][oy];
-        // fast path: z window of this stencil column.  Each lane's reach in z is
-        // sqrt(R^2 - dxy^2), dxy its xy distance to the column (geometric cell bounds in the
-        // staged image frame, padded); the warp tests only the staged atoms whose z lies in
-        // the union of the lanes' windows (cells are z-sorted, so that is a contiguous slice).
-        // R and the pads are far outside the fp32 rounding of d^2, so no accepted pair is cut.
-        float zlo = -INFINITY, zhi = INFINITY;
-        if (fast) {
+    // list tile layout: entries k of atom i at nbl[r][k / 8][i][k % 8]; each lane
+    // collects 8 entries in its shared-memory column and writes them as one 32-byte sector
+    uint4 *out = reinterpret_cast<uint4 *>(d.nbl + (size_t)r * kp.cap * kp.Nst) + 2 * (size_t)(valid ? i : 0);
+    const size_t ostride = 2 * (size_t)kp.Nst;                 // uint4 per 8-entry block row
+    int cnt = 0, flushed = 0;
+    // Flat walk over the stencil cells (ox, oy, oz).  Cell ranges come from shared memory
+    // and the next cell's first chunk of positions is loaded while the current one is
+    // tested, so the warp waits for one memory latency per rebuild instead of two per cell.
+    const int nyz = kp.ns[1] * kp.ns[2], nst = kp.ns[0] * nyz;
+    float4 pc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int tc = 0;
+    {
+      const int jb = s_jb[0];
+      if (lane < s_je[0] - jb) { pc = xq[jb + lane]; tc = meta[jb + lane].y; }
+    }
+    float zlo = -INFINITY, zhi = INFINITY;
+    for (int t = 0; t < nst; ++t) {
+      float4 pn = make_float4(0.f, 0.f, 0.f, 0.f);
+      int tn = 0;
+      if (t + 1 < nst) {
+        const int jb = s_jb[t + 1];
+        if (lane < s_je[t + 1] - jb) { pn = xq[jb + lane]; tn = meta[jb + lane].y; }
+      }
+      const int ox = t / nyz, oy = (t / kp.ns[2]) % kp.ns[1], oz = t % kp.ns[2];
+      const float wsx = s_wsh[0][ox], wsy = s_wsh[1][oy], wsz = s_wsh[2][oz];
+      bool skip = false;
+      if (fast) {
+        if (oz == 0) {
+          // z window of this stencil column.  Each lane's reach in z is sqrt(R^2 - dxy^2), dxy
+          // its xy distance to the column (geometric cell bounds in the staged image frame,
+          // padded); the warp tests only the staged atoms whose z lies in the union of the
+          // lanes' windows (cells are z-sorted, so that is a contiguous slice).  R and the pads
+          // are far outside the fp32 rounding of d^2, so no accepted pair is cut.
           const float xlo = (float)(cx - 2 + ox) * csx - kWinPad, xhi = xlo + csx + 2.f * kWinPad;
           const float ylo = (float)(cy - 2 + oy) * csy - kWinPad, yhi = ylo + csy + 2.f * kWinPad;
           const float ddx = fmaxf(0.f, fmaxf(xlo - xi.x, xi.x - xhi));
@@ -238,92 +269,107 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
             zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
             zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
           }
-          if (!(zlo <= zhi)) continue;   // no lane reaches this column (warp-uniform)
         }
-        for (int oz = 0; oz < kp.ns[2]; ++oz) {
-          if (fast) {
-            const float zc = (float)(cz - 2 + oz) * csz;
-            if (zhi < zc - kWinPad || zlo > zc + csz + kWinPad) continue;
+        const float zc = (float)(cz - 2 + oz) * csz;
+        skip = !(zlo <= zhi) || zhi < zc - kWinPad || zlo > zc + csz + kWinPad;
+      }
+      // accepted pairs' canonical image k = -(j-cell shift) (nearest image, r < L/2)
+      const int fast_code = (1 - s_wi[0][ox]) * 9 + (1 - s_wi[1][oy]) * 3 + (1 - s_wi[2][oz]);
+      const int jb = s_jb[t], je = s_je[t];
+      for (int j0 = jb; !skip && j0 < je; j0 += 32) {
+        const int nj = min(32, je - j0);
+        int tb = 0, te = nj;
+        float4 p = pc;
+        int ty = tc;
+        if (j0 != jb && lane < nj) { p = xq[j0 + lane]; ty = meta[j0 + lane].y; }   // cells > 32 atoms
+        __syncwarp();
+        {
+          float zt = 0.f;
+          if (lane < nj) {
+            // fast path: stage the j-cell's periodic image (uniform for a +-2 stencil)
+            sx[lane] = fast ? make_float4(p.x + wsx, p.y + wsy, p.z + wsz, 0.f) : p;
+            sj[lane] = (j0 + lane) | ((ty & (int)kEntryTypeMask) << kEntryTypeShift);
+            zt = p.z + wsz;
           }
-          const int cc = (gx * kp.nc[1] + gy) * kp.nc[2] + s_cell[2][oz];
-          const float wsz = s_wsh[2][oz];
-          // accepted pairs' canonical image k = -(j-cell shift) (nearest image, r < L/2)
-          const int fast_code = (1 - s_wi[0][ox]) * 9 + (1 - s_wi[1][oy]) * 3 + (1 - s_wi[2][oz]);
-          const int jb = start[cc], je = start[cc + 1];
-          for (int j0 = jb; j0 < je; j0 += 32) {
-            const int nj = min(32, je - j0);
-            int tb = 0, te = nj;
-            __syncwarp();
-            {
-              float zt = 0.f;
-              if (lane < nj) {
-                const int j = j0 + lane;
-                const float4 p = xq[j];
-                // fast path: stage the j-cell's periodic image (uniform for a +-2 stencil)
-                sx[lane] = fast ? make_float4(p.x + wsx, p.y + wsy, p.z + wsz, 0.f) : p;
-                sj[lane] = j | ((meta[j].y & (int)kEntryTypeMask) << kEntryTypeShift);
-                zt = p.z + wsz;
-              }
-              if (fast) {
-                tb = __popc(__ballot_sync(0xffffffffu, lane < nj && zt < zlo));
-                te = __popc(__ballot_sync(0xffffffffu, lane < nj && zt <= zhi));
-              }
-            }
-            __syncwarp();
-            if (!valid) continue;
-            for (int t0 = tb; t0 < te; t0 += 4) {
-              float d2v[4], kxv[4], kyv[4], kzv[4];
+          if (fast) {
+            tb = __popc(__ballot_sync(0xffffffffu, lane < nj && zt < zlo));
+            te = __popc(__ballot_sync(0xffffffffu, lane < nj && zt <= zhi));
+          }
+        }
+        __syncwarp();
+        if (!valid) continue;
+        for (int t0 = tb; t0 < te; t0 += 4) {
+          float d2v[4], kxv[4], kyv[4], kzv[4];
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const float4 xj = sx[min(t0 + u, te - 1)];
-                if (fast) {
-                  // approximate d^2 from the staged image; exact canonical decision below
-                  // only for the rare candidates within the rounding band of r_list^2
-                  const float dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
-                  d2v[u] = dx * dx + dy * dy + dz * dz;
-                } else {
-                  // canonical formula (R14): dx = x_j - x_i ; dx -= L rint(dx / L);
-                  // positions are wrapped into [0, L] at the rebuild, so |dx / L| <= 1 and
-                  // rint(t) == (t > 0.5) - (t < -0.5) exactly (ties to even)
-                  const float rx = __fsub_rn(xj.x, xi.x), ry = __fsub_rn(xj.y, xi.y), rz = __fsub_rn(xj.z, xi.z);
-                  kxv[u] = rint_unit(__fmul_rn(rx, Linv.x));
-                  kyv[u] = rint_unit(__fmul_rn(ry, Linv.y));
-                  kzv[u] = rint_unit(__fmul_rn(rz, Linv.z));
-                  const float dx = __fsub_rn(rx, __fmul_rn(Lbox.x, kxv[u]));
-                  const float dy = __fsub_rn(ry, __fmul_rn(Lbox.y, kyv[u]));
-                  const float dz = __fsub_rn(rz, __fmul_rn(Lbox.z, kzv[u]));
-                  d2v[u] = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-                }
-              }
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                if (t0 + u >= te) continue;
-                int code;
-                if (fast) {
-                  if (d2v[u] >= hi2) continue;
-                  if (d2v[u] >= lo2 && !canonical_in(xq[sj[t0 + u] & (int)kEntryJMask], xi, Lbox, Linv, rlist2)) continue;
-                  code = fast_code;
-                } else {
-                  if (!(d2v[u] < rlist2)) continue;
-                  code = (int)(kxv[u] * 9.0f + kyv[u] * 3.0f + kzv[u]) + 13;
-                }
-                const int je_ = sj[t0 + u] | (code << kEntryImgShift);
-                const int j = je_ & (int)kEntryJMask;
-                if (j == i) continue;
-                if (ee > eb) {
-                  const int oj = meta[j].x;
-                  bool ex = false;
-                  for (int e = eb; e < ee; ++e) ex |= (d.excl_idx[e] == oj);
-                  if (ex) continue;
-                }
-                if (cnt < kp.cap) *out = (uint32_t)je_;
-                out += ostride;
-                ++cnt;
-              }
+          for (int u = 0; u < 4; ++u) {
+            const float4 xj = sx[min(t0 + u, te - 1)];
+            if (fast) {
+              // approximate d^2 from the staged image; exact canonical decision below
+              // only for the rare candidates within the rounding band of r_list^2
+              const float dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
+              d2v[u] = dx * dx + dy * dy + dz * dz;
+            } else {
+              // canonical formula (R14): dx = x_j - x_i ; dx -= L rint(dx / L);
+              // positions are wrapped into [0, L] at the rebuild, so |dx / L| <= 1 and
+              // rint(t) == (t > 0.5) - (t < -0.5) exactly (ties to even)
+              const float rx = __fsub_rn(xj.x, xi.x), ry = __fsub_rn(xj.y, xi.y), rz = __fsub_rn(xj.z, xi.z);
+              kxv[u] = rint_unit(__fmul_rn(rx, Linv.x));
+              kyv[u] = rint_unit(__fmul_rn(ry, Linv.y));
+              kzv[u] = rint_unit(__fmul_rn(rz, Linv.z));
+              const float dx = __fsub_rn(rx, __fmul_rn(Lbox.x, kxv[u]));
+              const float dy = __fsub_rn(ry, __fmul_rn(Lbox.y, kyv[u]));
+              const float dz = __fsub_rn(rz, __fmul_rn(Lbox.z, kzv[u]));
+              d2v[u] = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
             }
+          }
+          // each lane appends accepted entries to its 16-entry shared-memory ring and writes a
+          // full 8-entry tile (one 32-byte sector) at most once per 4 candidates
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (t0 + u >= te) continue;
+            int code;
+            if (fast) {
+              if (d2v[u] >= hi2) continue;
+              if (d2v[u] >= lo2 && !canonical_in(xq[sj[t0 + u] & (int)kEntryJMask], xi, Lbox, Linv, rlist2)) continue;
+              code = fast_code;
+            } else {
+              if (!(d2v[u] < rlist2)) continue;
+              code = (int)(kxv[u] * 9.0f + kyv[u] * 3.0f + kzv[u]) + 13;
+            }
+            const int je_ = sj[t0 + u] | (code << kEntryImgShift);
+            const int j = je_ & (int)kEntryJMask;
+            if (j == i) continue;
+            if (ee > eb) {                    // solute atoms only
+              const int oj = meta[j].x;
+              bool ex = false;
+              for (int e = eb; e < ee; ++e) ex |= (d.excl_idx[e] == oj);
+              if (ex) continue;
+            }
+            s_buf[cnt & 15][lane] = (uint32_t)je_;
+            ++cnt;
+          }
+          if (cnt - flushed >= 8) {
+            if (flushed < kp.cap) {
+              const int h = flushed & 8;
+              out[0] = make_uint4(s_buf[h][lane], s_buf[h + 1][lane], s_buf[h + 2][lane], s_buf[h + 3][lane]);
+              out[1] = make_uint4(s_buf[h + 4][lane], s_buf[h + 5][lane], s_buf[h + 6][lane], s_buf[h + 7][lane]);
+              out += ostride;
+            }
+            flushed += 8;
           }
         }
       }
+      pc = pn;
+      tc = tn;
+    }
+    if (valid && cnt > flushed && flushed < kp.cap) {
+      // pad the last tile with the atom's own slot (zero shift, r = 0: skipped by the pair kernel)
+      const uint32_t self = (uint32_t)i | ((uint32_t)(meta[i].y & (int)kEntryTypeMask) << kEntryTypeShift) |
+                            (13u << kEntryImgShift);
+      const int h = flushed & 8;
+      for (int k = cnt - flushed; k < 8; ++k) s_buf[h + k][lane] = self;
+      out[0] = make_uint4(s_buf[h][lane], s_buf[h + 1][lane], s_buf[h + 2][lane], s_buf[h + 3][lane]);
+      out[1] = make_uint4(s_buf[h + 4][lane], s_buf[h + 5][lane], s_buf[h + 6][lane], s_buf[h + 7][lane]);
     }
     if (valid) {
       d.nnb[base + i] = cnt;

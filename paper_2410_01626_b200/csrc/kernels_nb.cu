@@ -25,33 +25,29 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
   const float qif = kp.fcoul * xi.w;
   float fx = 0.f, fy = 0.f, fz = 0.f, phi = 0.f;
   double phid = 0.0, elj = 0.0;        // fp64 only in lambda warps / on energy steps
-  const uint32_t *L = d.nbl + (size_t)r * kp.cap * kp.Nst + i;
+  // 8-entry tiles nbl[k/8][i][k%8] (kernels_list.cu): one 16-byte load per 4 neighbours; the
+  // builder pads a lane's last tile with its own slot
+  const uint4 *L = reinterpret_cast<const uint4 *>(d.nbl + (size_t)r * kp.cap * kp.Nst) + 2 * (size_t)i;
+  const size_t tstride = 2 * (size_t)kp.Nst;
   const float2 *ljrow = ljf + ti * kp.T;
   const float2 *ljerow = lje + ti * kp.T;
   const float rc2 = kp.rc2, beta = kp.beta, c2b = kp.two_beta_sqrtpi;
   const float kexp = -kp.beta * kp.beta * 1.4426950408889634f;   // exp(-b^2 r^2) = 2^(kexp r^2)
   const float pbeta = kErfcP * kp.beta;
-  constexpr int U = 4;                 // neighbours in flight per lane
-  // Entries past a lane's own count point at the lane's own atom with zero shift (r2 = 0,
-  // masked), so a chunk's U loads are unconditional and the next chunk's entries are
-  // prefetched while the current chunk computes.
+  constexpr int U = 4;                 // neighbours in flight per lane (half a list tile)
+  // Entries past a lane's own (padded) count point at the lane's own atom with zero shift
+  // (r2 = 0, masked), so the loads are unconditional; a whole tile (32 bytes per lane, one
+  // sector) is fetched at once and the next tile is prefetched while this one computes.
   const uint32_t self = (uint32_t)(valid ? i : 0) | ((uint32_t)ti << kEntryTypeShift) |
                         (13u << kEntryImgShift);
-  uint32_t en[U];
-  const int stride = kp.Nst;
-#pragma unroll
-  for (int u = 0; u < U; ++u) en[u] = u < n ? __ldcs(L + u * stride) : self;
-  const uint32_t *Lk = L + U * stride;
-  for (int k0 = 0; k0 < nmax; k0 += U, Lk += U * stride) {
-    uint32_t e[U];
+  const uint4 selfv = make_uint4(self, self, self, self);
+  uint4 ta = selfv, tb = selfv;
+  if (n > 0) { ta = __ldcs(L); tb = __ldcs(L + 1); }
+  auto chunk = [&](const uint4 ev) {
+    const uint32_t e[U] = {ev.x, ev.y, ev.z, ev.w};
     float4 xj[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      e[u] = en[u];
-      xj[u] = __ldg(&xq[(int)(e[u] & kEntryJMask)]);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) en[u] = k0 + U + u < n ? __ldcs(Lk + u * stride) : self;
+    for (int u = 0; u < U; ++u) xj[u] = __ldg(&xq[(int)(e[u] & kEntryJMask)]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const float4 sh = shift[e[u] >> kEntryImgShift];
@@ -80,6 +76,20 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
         elj += in ? (double)(r6 * fmaf(ce.y, r6, -ce.x)) : 0.0;
       }
     }
+  };
+  for (int k0 = 0; k0 < nmax; k0 += 8) {
+    const uint4 ca = ta, cb = tb;
+    const int kn = k0 + 8;
+    if (kn < n) {
+      const uint4 *Lt = L + (size_t)(kn >> 3) * tstride;
+      ta = __ldcs(Lt);
+      tb = __ldcs(Lt + 1);
+    } else {
+      ta = selfv;
+      tb = selfv;
+    }
+    chunk(ca);
+    if (k0 + 4 < nmax) chunk(cb);
   }
   // exclusion corrections (solute atoms only; most atoms have none)
   float phx = 0.f;
@@ -146,7 +156,7 @@ __global__ void __launch_bounds__(128) k_nonbonded(KParams kp, DevBufs d, int st
   const int2 mi = d.meta[idx];
   const int ti = mi.y & 0xFF;
   const int lslot = valid ? (mi.y >> 8) - 1 : -1;
-  const int n = valid ? d.nnb[idx] : 0;
+  const int n = valid ? min(d.nnb[idx], kp.cap) : 0;   // overflow is flagged by the builder
   const int nmax = __reduce_max_sync(0xffffffffu, n);
   const bool warp_lam = __any_sync(0xffffffffu, lslot >= 0);
   const float4 *xq = d.xyzq + (size_t)r * kp.Nst;
