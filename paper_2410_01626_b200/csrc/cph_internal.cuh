@@ -189,6 +189,8 @@ struct Ctx {
 int launch_integrate(Ctx &c, cudaStream_t s, int do_open);       // BAOA (+ pending close); Bussi: BA + T A
 int launch_close(Ctx &c, cudaStream_t s, int kick);                // final half kick / KE
 int launch_rebuild(Ctx &c, cudaStream_t s);                        // sort + pair list
+int launch_sort(Ctx &c, cudaStream_t s);                           // cell sort + permutation
+int launch_build_list(Ctx &c, cudaStream_t s);                     // pair list of the sorted atoms
 int launch_nonbonded(Ctx &c, cudaStream_t s, int step_offset);
 int launch_spread(Ctx &c, cudaStream_t s);
 int launch_solve(Ctx &c, cudaStream_t s, int step_offset);

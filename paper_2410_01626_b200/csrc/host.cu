@@ -211,13 +211,16 @@ int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
   int k = 0;
   cudaStream_t s = c.stream;
   k += launch_integrate(c, s, 1);
-  if (rebuild) k += launch_rebuild(c, s);
+  static const bool serial_build = getenv("CPH_SERIAL_BUILD") != nullptr;   // A/B diagnostic
+  if (rebuild) k += serial_build ? launch_rebuild(c, s) : launch_sort(c, s);
   cudaStream_t sp = s;
   if (two_streams) {
     cudaEventRecord(c.ev_fork, s);
     cudaStreamWaitEvent(c.stream_pme, c.ev_fork, 0);
     sp = c.stream_pme;
   }
+  // the PME chain needs only the sorted atoms: it overlaps the list build
+  if (rebuild && !serial_build) k += launch_build_list(c, s);
   cufftSetStream(c.plan_r2c, sp);
   cufftSetStream(c.plan_c2r, sp);
   k += launch_spread(c, sp);

@@ -381,7 +381,10 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
   }
 }
 
-int launch_rebuild(Ctx &c, cudaStream_t s) {
+// spatial sort + permutation of every per-atom array (positions wrapped); the pair list
+// itself is launch_build_list, so work that only needs the new atom order (the PME chain) can
+// start while the list is built
+int launch_sort(Ctx &c, cudaStream_t s) {
   const KParams &kp = c.kp;
   dim3 ga((kp.N + 127) / 128, kp.R);
   cudaMemsetAsync(c.d.cell_count, 0, sizeof(int) * (size_t)kp.R * kp.ncell, s);
@@ -391,8 +394,14 @@ int launch_rebuild(Ctx &c, cudaStream_t s) {
   k_cell_sort<<<dim3((kp.ncell + 127) / 128, kp.R), 128, 0, s>>>(kp, c.d);
   k_permute<<<ga, 128, 0, s>>>(kp, c.d);
   k_copy_back<<<ga, 128, 0, s>>>(kp, c.d);
-  k_build_list<<<dim3(kp.ncell, kp.R), 32, 0, s>>>(kp, c.d);
-  return 7;
+  return 6;
 }
+
+int launch_build_list(Ctx &c, cudaStream_t s) {
+  k_build_list<<<dim3(c.kp.ncell, c.kp.R), 32, 0, s>>>(c.kp, c.d);
+  return 1;
+}
+
+int launch_rebuild(Ctx &c, cudaStream_t s) { return launch_sort(c, s) + launch_build_list(c, s); }
 
 }  // namespace cph
