@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
               // approximate d^2 from the staged image; exact canonical decision below
               // only for the rare candidates within the rounding band of r_list^2
               const float dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
-              d2v[u] = dx * dx + dy * dy + dz * dz;
+              d2v[u] = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));   // within the band
             } else {
               // canonical formula (R14): dx = x_j - x_i ; dx -= L rint(dx / L);
               // positions are wrapped into [0, L] at the rebuild, so |dx / L| <= 1 and
