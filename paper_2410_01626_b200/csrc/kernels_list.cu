@@ -160,6 +160,11 @@ __global__ void k_copy_back(KParams kp, DevBufs d) {
 // One warp per cell: the i atoms are the cell's atoms (one per lane, chunks of 32), and every
 // stencil cell's atoms are staged through shared memory (coalesced loads, broadcast reads),
 // so the loop structure is uniform across the warp.
+// Fast-path (5x5x5) stencil walk: columns by ring around the i-cell's column, cells of a
+// column centre-out, so the far cells - whose pairs mostly end up beyond r_c - form the tail
+// of every atom's list and the pair kernel's warps skip their Ewald block together.
+__constant__ int c_walk[125] = {62, 61, 63, 60, 64, 37, 36, 38, 35, 39, 57, 56, 58, 55, 59, 67, 66, 68, 65, 69, 87, 86, 88, 85, 89, 32, 31, 33, 30, 34, 42, 41, 43, 40, 44, 82, 81, 83, 80, 84, 92, 91, 93, 90, 94, 12, 11, 13, 10, 14, 52, 51, 53, 50, 54, 72, 71, 73, 70, 74, 112, 111, 113, 110, 114, 7, 6, 8, 5, 9, 17, 16, 18, 15, 19, 27, 26, 28, 25, 29, 47, 46, 48, 45, 49, 77, 76, 78, 75, 79, 97, 96, 98, 95, 99, 107, 106, 108, 105, 109, 117, 116, 118, 115, 119, 2, 1, 3, 0, 4, 22, 21, 23, 20, 24, 102, 101, 103, 100, 104, 122, 121, 123, 120, 124};
+
 // padding of the geometric cell bounds and of the z-window radius (nm): >> the fp32
 // rounding of wrapped positions (|x| <= L ~ 14 nm, ulp ~ 1e-6)
 constexpr float kWinPad = 1e-4f;
@@ -208,7 +213,8 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
   {
     const int nyz = kp.ns[1] * kp.ns[2], nst = kp.ns[0] * nyz;
     for (int t = lane; t < nst; t += 32) {
-      const int ox = t / nyz, oy = (t / kp.ns[2]) % kp.ns[1], oz = t % kp.ns[2];
+      const int w = fast ? c_walk[t] : t;
+      const int ox = w / nyz, oy = (w / kp.ns[2]) % kp.ns[1], oz = w % kp.ns[2];
       const int cc = (s_cell[0][ox] * kp.nc[1] + s_cell[1][oy]) * kp.nc[2] + s_cell[2][oz];
       s_jb[t] = start[cc];
       s_je[t] = start[cc + 1];
@@ -244,11 +250,12 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
         const int jb = s_jb[t + 1];
         if (lane < s_je[t + 1] - jb) { pn = xq[jb + lane]; tn = meta[jb + lane].y; }
       }
-      const int ox = t / nyz, oy = (t / kp.ns[2]) % kp.ns[1], oz = t % kp.ns[2];
+      const int w = fast ? c_walk[t] : t;
+      const int ox = w / nyz, oy = (w / kp.ns[2]) % kp.ns[1], oz = w % kp.ns[2];
       const float wsx = s_wsh[0][ox], wsy = s_wsh[1][oy], wsz = s_wsh[2][oz];
       bool skip = false;
       if (fast) {
-        if (oz == 0) {
+        if (t % 5 == 0) {                // first cell of a column in the walk
           // z window of this stencil column.  Each lane's reach in z is sqrt(R^2 - dxy^2), dxy
           // its xy distance to the column (geometric cell bounds in the staged image frame,
           // padded); the warp tests only the staged atoms whose z lies in the union of the
