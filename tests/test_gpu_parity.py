@@ -295,3 +295,27 @@ def test_pfc_saturation_matches_oracle(cph):
     for r in range(3):
         ref = [OPFC.pfc_2state(6.0, s.pKa[0, 0], pH[r], 300.0, 1e6), *OPFC.pfc_3state(6.0, s.pKa[1], pH[r], 300.0, 1e6)]
         np.testing.assert_allclose(ctx.cph_get_bias_params(r), ref, atol=1e-7)
+
+
+def test_bench_launch_configuration_parity(cph):
+    """The exact configuration bench.py times (C2, 17 pH replicas in one context on a
+    dedicated stream, bench seeds and velocities), after a CUDA-graph block of steps: the
+    first and last replica against the oracle evaluated at the device state."""
+    import torch
+    s = make_system(2)
+    R = 17
+    pH = np.resize(np.asarray(s.pH_grid, np.float64), R)
+    seeds = replica_seeds(2, R, base=0)
+    vel = np.stack([make_velocities(s, r) for r in range(R)])
+    stream = torch.cuda.Stream()
+    ctx = cph.cph_create(s, pH, seeds, vel_replicas=vel, cuda_stream=stream.cuda_stream)
+    ctx.cph_step(20)
+    for r in (0, R - 1):
+        x, v = ctx.cph_get_positions(r)
+        lam, lamv = ctx.cph_get_lambdas(r)
+        ref = OracleReplica(s, pH[r], int(seeds[r]), lam0=lam, vel0=v, pos0=x)
+        ref.lamv = lamv
+        err = compare_snapshot(ctx, r, ref, lam_atoms=s.group_atoms)
+        print(r, {k: v for k, v in err.items() if k != "E_terms"})
+        assert err["force"] <= RTOL and err["phi"] <= RTOL and err["dvdl_coul"] <= RTOL
+        assert err["dvdl_bias"] <= 1e-9 and err["E_total"] <= ETOL, err["E_terms"]
