@@ -107,14 +107,39 @@ __device__ __forceinline__ bool canonical_in(float4 xj, float4 xi, float3 Lbox, 
   return __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz)) < rlist2;
 }
 
-__global__ void k_cell_sort(KParams kp, DevBufs d) {
-  const int r = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
+// one warp per cell: bitonic sort of the 64-bit keys (wrapped z bits, original index) with
+// register shuffles for cells of up to 32 atoms; larger cells (rare) fall back to an
+// insertion sort by lane 0.  Keys are unique, so the order is deterministic.
+__global__ void __launch_bounds__(128) k_cell_sort(KParams kp, DevBufs d) {
+  const int r = blockIdx.y, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (c >= kp.ncell) return;
   const int *start = d.cell_start + (size_t)r * (kp.ncell + 1);
   int *p = d.perm_tmp + (size_t)r * kp.Nst;
   const int2 *meta = d.meta + (size_t)r * kp.Nst;
   const float4 *xq = d.xyzq + (size_t)r * kp.Nst;
-  const int b = start[c], e = start[c + 1];
+  const int b = start[c], e = start[c + 1], n = e - b;
+  if (n <= 1) return;
+  if (n <= 32) {
+    unsigned long long key = ~0ull;
+    int v = 0;
+    if (lane < n) {
+      v = p[b + lane];
+      const float zw = wrap_coord(xq[v].z, kp.L[2], kp.invL[2]);     // >= 0: bits order like values
+      key = ((unsigned long long)__float_as_uint(zw) << 32) | (uint32_t)meta[v].x;
+    }
+    for (int k = 2; k <= 32; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, j);
+        const int ov = __shfl_xor_sync(0xffffffffu, v, j);
+        const bool lower = (lane & j) == 0, up = (lane & k) == 0;
+        const bool take = lower == up ? other < key : other > key;   // keep min on the low side
+        if (take) { key = other; v = ov; }
+      }
+    if (lane < n) p[b + lane] = v;
+    return;
+  }
+  if (lane) return;
   for (int a = b + 1; a < e; ++a) {
     const int v = p[a];
     const float kz = wrap_coord(xq[v].z, kp.L[2], kp.invL[2]);
@@ -398,7 +423,7 @@ int launch_sort(Ctx &c, cudaStream_t s) {
   k_cell_assign<<<ga, 128, 0, s>>>(kp, c.d);
   k_cell_scan<<<kp.R, 1024, 0, s>>>(kp, c.d);
   k_cell_scatter<<<ga, 128, 0, s>>>(kp, c.d);
-  k_cell_sort<<<dim3((kp.ncell + 127) / 128, kp.R), 128, 0, s>>>(kp, c.d);
+  k_cell_sort<<<dim3((kp.ncell + 3) / 4, kp.R), 128, 0, s>>>(kp, c.d);
   k_permute<<<ga, 128, 0, s>>>(kp, c.d);
   k_copy_back<<<ga, 128, 0, s>>>(kp, c.d);
   return 6;
