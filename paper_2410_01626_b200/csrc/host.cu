@@ -1267,7 +1267,7 @@ cph_status cph_get_forces(cph_ctx *ctx, int32_t r, float *f, float *phi) {
       f[3 * o + 2] = nb[s].z + rec[s].z;
     }
     if (phi) {
-      if (ls >= 0) phi[o] = (float)plam[ls];
+      if (ls >= 0) phi[o] = (float)(plam[ls] + phinet);   // kernel phi excludes the net-charge term
       else phi[o] = (float)((double)nb[s].w + (double)rec[s].w + selfc * xq[s].w + phinet);
     }
   }

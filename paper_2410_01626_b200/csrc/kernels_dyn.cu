@@ -195,22 +195,19 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
   const double V = kp.Ld[0] * kp.Ld[1] * kp.Ld[2];
   const double sqrtpi = 1.7724538509055160273;
 
-  // total charge and sum of squares
-  double qs = 0.0, qq = 0.0;
-  for (int k = threadIdx.x; k < kp.nlam; k += blockDim.x) {
-    const double q = d.qlam[(size_t)r * kp.nlam + k];
-    qs += q; qq += q * q;
-  }
-  const double Q = kp.Q_fixed + block_sum_d(qs);
-  const double Q2 = kp.Q2_fixed + block_sum_d(qq);
-  // per lambda atom (one thread each): full potential (real + excl + recip + self + net) and
-  // its products with dq/dlp, dq/dlt, staged in shared memory for the per-group sums
+  // per lambda atom (one thread each): potential (real + excl + recip + self) and its
+  // products with dq/dlp, dq/dlt, staged in shared memory for the per-group sums.  The
+  // net-charge term -pi Q/(V beta^2) is the same for every atom and every group's charge is
+  // constant in lambda (sum_i dq_i/dlambda = 0, checked at create), so it adds nothing to
+  // dV/dlambda; it enters the energies and cph_get_forces' phi only.
   extern __shared__ double s_dq[];            // [2 * nlam]
+  double qs = 0.0, qq = 0.0;                  // total lambda charge and sum of squares
   for (int k = threadIdx.x; k < kp.nlam; k += blockDim.x) {
     const size_t ix = (size_t)r * kp.nlam + k;
     const double q = d.qlam[ix];
-    const double phi = d.phi64_nb[ix] + d.phi64_rec[ix] - 2.0 * kp.beta_d / sqrtpi * q -
-                       kPi * Q / (V * kp.beta_d * kp.beta_d);
+    qs += q;
+    qq += q * q;
+    const double phi = d.phi64_nb[ix] + d.phi64_rec[ix] - 2.0 * kp.beta_d / sqrtpi * q;
     d.phi_lam[ix] = phi;
     const int g = d.k_group[k];
     const size_t ic = (size_t)r * kp.C + d.g_cptr[g];
@@ -246,7 +243,15 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
       d.dvdl_bias[ic + 1] = bt;
     }
   }
-  ebias = block_sum_d(ebias);   // includes __syncthreads: dV/dlambda visible to the block
+  // dV/dlambda visible to the block; the reductions only on energy steps
+  double Q = 0.0, Q2 = 0.0;
+  if (energy) {
+    ebias = block_sum_d(ebias);
+    Q = kp.Q_fixed + block_sum_d(qs);
+    Q2 = kp.Q2_fixed + block_sum_d(qq);
+  } else {
+    __syncthreads();
+  }
   // closing half kick, frames, TI accumulation, divergence
   double kel = 0.0;
   const bool frame = (m % kp.nstout) == 0 && (mode == 1 || (m == 0 && d.frame_total[r] == 0));
@@ -283,7 +288,7 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
     if (!dyn && mode == 1) d.ti_sum[ix] += d.dvdl_coul[ix];   // <dV_coul/dlambda>
     if (!(fabs(l) <= 10.0) || !isfinite(dv)) atomicOr(&d.flags[FLAG_DIVERGED], 1);
   }
-  kel = block_sum_d(kel);
+  if (energy) kel = block_sum_d(kel);
   if (threadIdx.x == 0) {
     if (frame) {
       d.frame_step[(size_t)r * kp.fcap + fslot] = m;
