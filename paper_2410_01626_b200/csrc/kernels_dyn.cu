@@ -257,6 +257,9 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
   const bool frame = (m % kp.nstout) == 0 && (mode == 1 || (m == 0 && d.frame_total[r] == 0));
   long long fslot = 0;
   if (frame) fslot = d.frame_total[r] % kp.fcap;
+  // the next step's opening is fused into this loop when no block-wide quantity needs the
+  // closed state first (Bussi's kinetic energy, DBO's protonation class of lambda_t)
+  const bool fuse_open = mode == 1 && dyn && m != end && !kp.bussi && !kp.dbo_on;
   for (int c = threadIdx.x; c < kp.C; c += blockDim.x) {
     const size_t ix = (size_t)r * kp.C + c;
     const double dv = d.dvdl_coul[ix] + d.dvdl_bias[ix];
@@ -287,6 +290,16 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
     }
     if (!dyn && mode == 1) d.ti_sum[ix] += d.dvdl_coul[ix];   // <dV_coul/dlambda>
     if (!(fabs(l) <= 10.0) || !isfinite(dv)) atomicOr(&d.flags[FLAG_DIVERGED], 1);
+    if (fuse_open) {
+      // next step's B A O A with the same force (Langevin; see lambda_open)
+      const double h = kp.dtd;
+      v += 0.5 * h * (-dv) / kp.m_lam;                                          // B
+      double ln = l + 0.5 * h * v;                                              // A
+      v = kp.c1_lam * v + kp.sd_lam * lambda_normal(d.seed[r], (uint32_t)m, (uint32_t)c);   // O
+      ln += 0.5 * h * v;                                                        // A
+      d.lamv[ix] = v;
+      d.lam[ix] = ln;
+    }
   }
   if (energy) kel = block_sum_d(kel);
   if (threadIdx.x == 0) {
@@ -305,7 +318,8 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
   }
   __syncthreads();
   if (mode == 1) {
-    if (dyn && m != end) lambda_open(kp, d, r, m);
+    if (fuse_open) lambda_set_charges(kp, d, r);
+    else if (dyn && m != end) lambda_open(kp, d, r, m);
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
