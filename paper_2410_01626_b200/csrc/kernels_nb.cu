@@ -131,9 +131,12 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
   }
 }
 
-__global__ void __launch_bounds__(128) k_nonbonded(KParams kp, DevBufs d, int step_offset) {
-  __shared__ float2 s_ljf[kMaxTypes * kMaxTypes];   // (6 c6, 12 c12) for forces
-  __shared__ float2 s_lje[kMaxTypes * kMaxTypes];   // (c6, c12) for energies
+__global__ void __launch_bounds__(128, 7) k_nonbonded(KParams kp, DevBufs d, int step_offset) {
+  // LJ tables sized T*T (dynamic shared memory): the rest of the SM's 256 KB stays L1 cache
+  // for the neighbour-position gathers
+  extern __shared__ float2 s_lj[];
+  float2 *s_ljf = s_lj;                              // (6 c6, 12 c12) for forces
+  float2 *s_lje = s_lj + kp.T * kp.T;                // (c6, c12) for energies
   __shared__ float4 s_shift[27];                    // image shift L * (kx, ky, kz)
   for (int t = threadIdx.x; t < kp.T * kp.T; t += blockDim.x) {
     const float2 c = d.ljtab[t];
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(128) k_nonbonded(KParams kp, DevBufs d, int st
 
 int launch_nonbonded(Ctx &c, cudaStream_t s, int step_offset) {
   dim3 grid((c.kp.N + 127) / 128, c.kp.R);
-  k_nonbonded<<<grid, 128, 0, s>>>(c.kp, c.d, step_offset);
+  k_nonbonded<<<grid, 128, 2 * sizeof(float2) * c.kp.T * c.kp.T, s>>>(c.kp, c.d, step_offset);
   return 1;
 }
 
