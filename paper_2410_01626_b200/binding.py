@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcph.so")
+LIB_PATH = os.environ.get("CPH_LIB", os.path.join(_HERE, "libcph.so"))   # CPH_LIB: A/B builds
 
 CPH_ABI_VERSION = 2
 STATUS = {0: "CPH_OK", 1: "CPH_E_INVALID", 2: "CPH_E_CUDA", 3: "CPH_E_DIVERGED", 4: "CPH_E_STATE",
