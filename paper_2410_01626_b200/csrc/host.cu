@@ -829,6 +829,25 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   c.host_step = 0;
   cph_status st = evaluate_here(c);
   if (st == CPH_OK) st = check_flags(c);
+  // a denser-than-average region overflowed the list capacity: grow it once (with margin)
+  // and rebuild; an overflow during stepping is reported by the next call instead
+  if (st == CPH_E_STATE && c.cap_grow > (size_t)kp.cap) {
+    const int newcap = (int)((c.cap_grow * 5 / 4 + 64 + 7) / 8 * 8);
+    void *old = c.d.nbl;
+    c.allocations.erase(std::remove(c.allocations.begin(), c.allocations.end(), old), c.allocations.end());
+    if (c.dev_free) c.dev_free(old, c.alloc_ctx); else cudaFree(old);
+    kp.cap = newcap;
+    d.nbl = dalloc<uint32_t>(c, RN * kp.cap);
+    if (!d.nbl) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
+    const int zero[FLAG_COUNT] = {0};
+    if (cudaMemcpy(d.flags, zero, sizeof(zero), cudaMemcpyHostToDevice) != cudaSuccess) {
+      c.err = "flag reset failed";
+      return fail_create(ctx, CPH_E_CUDA);
+    }
+    c.err.clear();
+    st = evaluate_here(c);
+    if (st == CPH_OK) st = check_flags(c);
+  }
   if (st != CPH_OK) {
     cph_status s2 = st;
     if (c.plan_r2c) cufftDestroy(c.plan_r2c);

@@ -319,3 +319,29 @@ def test_bench_launch_configuration_parity(cph):
         print(r, {k: v for k, v in err.items() if k != "E_terms"})
         assert err["force"] <= RTOL and err["phi"] <= RTOL and err["dvdl_coul"] <= RTOL
         assert err["dvdl_bias"] <= 1e-9 and err["E_total"] <= ETOL, err["E_terms"]
+
+
+def test_dense_region_grows_list_capacity_and_no_groups(cph):
+    """Edge cases: a system with no lambda-groups whose solvent is squeezed into 0.6^3 of the
+    box (4.6x the mean density: up to 601 neighbours against the default capacity of 1.6x the
+    mean count + 64 = 512): create grows the capacity, the pair list stays bit-exact and the
+    forces match the oracle."""
+    import copy
+    s = copy.deepcopy(small_system(n_solvent=600, his=False))
+    s.group_kind = s.group_kind[:0]
+    s.group_ptr = s.group_ptr[:1]
+    s.group_atoms = s.group_atoms[:0]
+    s.state_q = s.state_q[:0]
+    s.is_buffer = s.is_buffer[:0]
+    s.pKa = s.pKa[:0]
+    s.vmm = s.vmm[:0]
+    mob = s.mass > 0
+    s.pos[mob] = (s.pos[mob] % s.box) * 0.6
+    ctx = cph.cph_create(s, [4.4], [3])
+    got = ctx.cph_get_pairlist(0)
+    ref = OPL.canonical_pairs(s.pos, s.box, s.params["rlist"], s.excl)
+    assert np.array_equal(got, ref)
+    oref = OracleReplica(s, 4.4, 3, lam0=np.zeros(0))
+    err = compare_snapshot(ctx, 0, oref)
+    print({k: v for k, v in err.items() if k != "E_terms"})
+    assert err["force"] <= RTOL and err["phi"] <= RTOL
