@@ -205,7 +205,10 @@ typedef struct {
 void cph_default_params(cph_params *p);
 
 /* Validate, copy to the device, run the PFC for every replica's pH, build the
- * pair list and evaluate forces/potentials/energies at step 0.
+ * pair list and evaluate forces/potentials/energies at step 0.  The pair-list
+ * capacity per atom is 1.6x the mean neighbour count + 64, grown once here if the
+ * initial configuration exceeds it; an overflow at a later rebuild is latched and
+ * reported as CPH_E_STATE by the next call.
  * CPH_E_INVALID: non-finite input, bad sizes, a group whose total charge
  * varies with lambda, rlist >= min(box)/2, rc > rlist.
  * CPH_E_UNSUPPORTED: pme_order != 4, grid not even / not 2,3,5,7-smooth. */
