@@ -242,14 +242,16 @@ def test_gpu_sampling_follows_hh_when_coulomb_dvdl_vanishes(cph):
     assert np.all(np.abs(his_e - prot * 10 ** (levels - pk_e)) < 0.03)
 
 
-def test_full_size_c5_sampled_parity(cph):
-    """BASELINE's largest config (250k atoms, K=128) in the bench launch configuration: sampled
-    atoms' phi and forces and every group's dV/dlambda against the oracle computed one by one."""
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_full_size_sampled_parity(cph, cfg):
+    """BASELINE's large configs (C3 25k atoms / 15 groups, C4 40k / 20 groups incl. His, C5
+    250k / 150 groups, K = 60 / 72 / 128) at full size: sampled atoms' phi and forces and every
+    group's dV/dlambda against the oracle computed one by one."""
     from oracle import ewald as OE
     from oracle import pme as OP
     from oracle.charges import charges
     from oracle.units import F_COUL
-    s = make_system(5)
+    s = make_system(cfg)
     lam0 = np.random.default_rng(2).uniform(0, 1, (1, s.n_coords))
     ctx = cph.cph_create(s, [5.0], [11], lambda0=lam0)
     f, phi = ctx.cph_get_forces(0)
@@ -283,7 +285,7 @@ def test_full_size_c5_sampled_parity(cph):
                 ref[cp[g] + 1] += F_COUL * dq[k, 1] * p
                 mag[cp[g] + 1] += abs(F_COUL * dq[k, 1] * p)
     err = np.abs(coul - ref) / np.maximum(np.abs(ref), mag)
-    print("C5 dvdl max rel", err.max())
+    print(f"C{cfg} dvdl max rel", err.max())
     assert err.max() < 2e-5
 
 

@@ -119,3 +119,35 @@ def test_replica_exchange_sampling_keeps_per_ph_populations(cph):
     # standard errors over ladders are ~0.01 at this length (tools/diag_remd_pop.py)
     assert np.all(np.abs(frac - hh) < 0.04)
     assert np.all(b.sum(0) > 0.1 * a.sum(0))
+
+
+def test_two_contexts_exchange_like_one(cph):
+    """The multi-GPU layout on one device: two contexts holding replicas [0, 3) and [3, 6) of
+    one 6-replica ladder (remd_first / remd_total), rows concatenated as the NCCL all-gather
+    would, take exactly the decisions of a single context holding all six."""
+    import torch
+    s = small_system()
+    levels = np.array([3.5, 4.0, 4.5, 5.0, 5.5, 6.0])
+    labels = np.array([2, 0, 5, 1, 4, 3])
+    rng = np.random.default_rng(12)
+    lam0 = rng.uniform(0.0, 1.0, (6, 3))
+    seeds = replica_seeds(8, 6)
+    one = cph.cph_create(s, levels[labels], seeds, lambda0=lam0, ph_levels=levels)
+    a = cph.cph_create(s, levels[labels[:3]], seeds[:3], lambda0=lam0[:3], ph_levels=levels, remd_first=0,
+                       remd_total=6)
+    b = cph.cph_create(s, levels[labels[3:]], seeds[3:], lambda0=lam0[3:], ph_levels=levels, remd_first=3,
+                       remd_total=6)
+    for attempt in range(12):
+        rows = torch.empty(6 * 7, dtype=torch.float64, device="cuda")
+        a.exchange_energies_into(rows[:21])
+        b.exchange_energies_into(rows[21:])
+        a.exchange_apply_from(rows, 5, attempt)
+        b.exchange_apply_from(rows, 5, attempt)
+        one.cph_exchange(5, attempt)
+        np.testing.assert_array_equal(np.concatenate([a.cph_get_labels(), b.cph_get_labels()]),
+                                      one.cph_get_labels())
+    sa, ca = a.cph_get_exchange_stats(1)
+    so, co = one.cph_get_exchange_stats(1)
+    np.testing.assert_array_equal(sa, so)
+    np.testing.assert_array_equal(ca, co)
+    assert co.sum() > 0
