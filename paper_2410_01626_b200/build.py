@@ -24,6 +24,7 @@ SOURCES = {
     "kernels_dyn.cu": ["-ftz=true"],
     "kernels_remd.cu": [],
     "kernels_hi.cu": [],
+    "kernels_state.cu": [],
 }
 
 

@@ -30,7 +30,7 @@ constexpr int kMaxAtoms = 1 << 21;
 
 // Device-side flags (int array)
 enum { FLAG_PENDING_CLOSE = 0, FLAG_LIST_OVERFLOW = 1, FLAG_DIVERGED = 2, FLAG_MAX_NNB = 3,
-       FLAG_STEP_DONE = 4, FLAG_COUNT = 8 };
+       FLAG_STEP_DONE = 4, FLAG_BAD_STATE = 5, FLAG_COUNT = 8 };
 
 // Scalars every kernel needs, passed by value.
 struct KParams {
@@ -137,6 +137,7 @@ struct DevBufs {
   uint32_t *hi_excl = nullptr;                      // [nlam] intra-group exclusion mask per atom
   double *hi_M = nullptr;                           // [R*G*10] reciprocal form matrix (without f)
   float *hi_F = nullptr;                            // [R*nlam*3] reciprocal force sums (without 4 pi f)
+  char *state_buf = nullptr;                        // [R * state blob bytes] staging of get/set_state
   double *hi_dvdl = nullptr;                        // [R*C] dC/dlambda
 };
 
@@ -203,6 +204,10 @@ int launch_remd_apply(Ctx &c, cudaStream_t s, const double *rows_all, uint64_t s
 int launch_bias_refresh(Ctx &c, cudaStream_t s);
 int launch_hi_recip(Ctx &c, cudaStream_t s);
 int launch_hi_finish(Ctx &c, cudaStream_t s, int step_offset);
+// state blobs (original atom order) packed / checked / unpacked on the device
+int launch_pack_state(Ctx &c, cudaStream_t s, char *dst, long long one, int r0, int nr, long long step);
+int launch_check_state(Ctx &c, cudaStream_t s, const char *src, long long one, int nr);
+int launch_unpack_state(Ctx &c, cudaStream_t s, const char *src, long long one, int r0, int nr);
 
 // host PFC (pfc.cu); dw = (a0, a1, h_prot, h_deprot) of each coordinate of the site
 bool pfc_two_state(const double dw[4], double pKa, double pH, double T, double kw, double *d1, std::string *err);

@@ -1358,57 +1358,73 @@ cph_status cph_get_ti_means(cph_ctx *ctx, int32_t r, double *mean, int64_t *n_sa
 // blob: int64 magic, N, C, step | float pos[3N], vel[3N] | double lam[C], lamv[C]
 static const int64_t kMagic = 0x3148504331ll;
 
+static size_t state_bytes(const Ctx &c) {
+  return 4 * sizeof(int64_t) + 6 * (size_t)c.kp.N * sizeof(float) + 2 * (size_t)c.kp.C * sizeof(double);
+}
+
+static cph_status ensure_state_buf(Ctx &c) {
+  if (c.d.state_buf) return CPH_OK;
+  c.d.state_buf = dalloc<char>(c, state_bytes(c) * c.kp.R);
+  if (!c.d.state_buf) { c.err = "device allocation failed"; return CPH_E_OOM; }
+  return CPH_OK;
+}
+
+// replicas [r0, r0 + nr) -> host blobs (packed on the device, one copy)
+static cph_status get_states(Ctx &c, int r0, int nr, void *buf) {
+  cph_status st = ensure_state_buf(c);
+  if (st) return st;
+  const size_t one = state_bytes(c);
+  c.launches += launch_pack_state(c, c.stream, c.d.state_buf, (long long)one, r0, nr, c.host_step);
+  CK(cudaMemcpyAsync(buf, c.d.state_buf, one * nr, cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  return CPH_OK;
+}
+
+// host blobs -> replicas [r0, r0 + nr): headers checked on the host, finiteness on the device
+// before anything is overwritten; then TI restart and a fresh evaluation
+static cph_status set_states(Ctx &c, int r0, int nr, const void *buf, int64_t nbytes) {
+  const size_t one = state_bytes(c);
+  if (nbytes < (int64_t)(one * nr)) { c.err = "state blob too small"; return CPH_E_INVALID; }
+  for (int k = 0; k < nr; ++k) {
+    int64_t hdr[4];
+    std::memcpy(hdr, (const char *)buf + one * k, sizeof hdr);
+    if (hdr[0] != kMagic || hdr[1] != (int64_t)c.kp.N || hdr[2] != (int64_t)c.kp.C) {
+      c.err = "state blob does not match this context";
+      return CPH_E_INVALID;
+    }
+  }
+  cph_status st = ensure_state_buf(c);
+  if (st) return st;
+  CK(cudaMemcpyAsync(c.d.state_buf, buf, one * nr, cudaMemcpyHostToDevice, c.stream));
+  c.launches += launch_check_state(c, c.stream, c.d.state_buf, (long long)one, nr);
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, c.d.flags + FLAG_BAD_STATE, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  if (bad) {
+    const int zero = 0;
+    CK(cudaMemcpy(c.d.flags + FLAG_BAD_STATE, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    c.err = "non-finite state";
+    return CPH_E_INVALID;
+  }
+  c.launches += launch_unpack_state(c, c.stream, c.d.state_buf, (long long)one, r0, nr);
+  // a new configuration: TI accumulators restart
+  CK(cudaMemsetAsync(c.d.ti_sum, 0, sizeof(double) * (size_t)c.kp.R * c.kp.C, c.stream));
+  CK(cudaMemsetAsync(c.d.ti_n, 0, sizeof(long long), c.stream));
+  if ((st = evaluate_here(c))) return st;
+  return check_flags(c);
+}
+
 cph_status cph_get_state(cph_ctx *ctx, int32_t r, void *buf, int64_t cap, int64_t *n) {
   if (!ctx || !n) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
   if (st) return st;
-  const size_t N = c.kp.N, C = c.kp.C;
-  const size_t bytes = 4 * sizeof(int64_t) + 6 * N * sizeof(float) + 2 * C * sizeof(double);
-  *n = (int64_t)bytes;
+  *n = (int64_t)state_bytes(c);
   if (!buf) return CPH_OK;
-  if (cap < (int64_t)bytes) { c.err = "state buffer too small"; return CPH_E_INVALID; }
-  char *p = (char *)buf;
-  int64_t hdr[4] = {kMagic, (int64_t)N, (int64_t)C, c.host_step};
-  std::memcpy(p, hdr, sizeof hdr);
-  float *pos = (float *)(p + sizeof hdr);
-  if ((st = cph_get_positions(ctx, r, pos, pos + 3 * N))) return st;
-  double *lam = (double *)(pos + 6 * N);
-  return cph_get_lambdas(ctx, r, lam, lam + C);
-}
-
-static cph_status upload_state(Ctx &c, int32_t r, const void *buf, int64_t nbytes) {
-  const size_t N = c.kp.N, C = c.kp.C;
-  const size_t bytes = 4 * sizeof(int64_t) + 6 * N * sizeof(float) + 2 * C * sizeof(double);
-  int64_t hdr[4];
-  if (nbytes < (int64_t)bytes) { c.err = "state blob too small"; return CPH_E_INVALID; }
-  std::memcpy(hdr, buf, sizeof hdr);
-  if (hdr[0] != kMagic || hdr[1] != (int64_t)N || hdr[2] != (int64_t)C) {
-    c.err = "state blob does not match this context";
-    return CPH_E_INVALID;
-  }
-  const float *pos = (const float *)((const char *)buf + sizeof hdr);
-  const float *vel = pos + 3 * N;
-  const double *lam = (const double *)(vel + 3 * N);
-  if (!finite_arr(pos, 6 * N) || !finite_arr(lam, 2 * C)) { c.err = "non-finite state"; return CPH_E_INVALID; }
-  const size_t base = (size_t)r * c.kp.Nst;
-  std::vector<float4> xq(N), v(N);
-  std::vector<int2> meta(N);
-  CK(cudaMemcpy(xq.data(), c.d.xyzq + base, sizeof(float4) * N, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(v.data(), c.d.vel + base, sizeof(float4) * N, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(meta.data(), c.d.meta + base, sizeof(int2) * N, cudaMemcpyDeviceToHost));
-  for (size_t s = 0; s < N; ++s) {
-    const int o = meta[s].x;
-    xq[s].x = pos[3 * o]; xq[s].y = pos[3 * o + 1]; xq[s].z = pos[3 * o + 2];
-    if (v[s].w > 0.0f) { v[s].x = vel[3 * o]; v[s].y = vel[3 * o + 1]; v[s].z = vel[3 * o + 2]; }
-  }
-  CK(cudaMemcpy(c.d.xyzq + base, xq.data(), sizeof(float4) * N, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(c.d.vel + base, v.data(), sizeof(float4) * N, cudaMemcpyHostToDevice));
-  if (C) {
-    CK(cudaMemcpy(c.d.lam + (size_t)r * C, lam, sizeof(double) * C, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c.d.lamv + (size_t)r * C, lam + C, sizeof(double) * C, cudaMemcpyHostToDevice));
-  }
-  return CPH_OK;
+  if (cap < *n) { c.err = "state buffer too small"; return CPH_E_INVALID; }
+  cudaSetDevice(c.device);
+  if ((st = cph_sync(ctx))) return st;
+  return get_states(c, r, 1, buf);
 }
 
 cph_status cph_set_state(cph_ctx *ctx, int32_t r, const void *buf, int64_t nbytes) {
@@ -1416,42 +1432,28 @@ cph_status cph_set_state(cph_ctx *ctx, int32_t r, const void *buf, int64_t nbyte
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
   if (st || (st = cph_sync(ctx))) return st;
-  if ((st = upload_state(c, r, buf, nbytes))) return st;
-  // a new configuration: TI accumulators restart
-  CK(cudaMemsetAsync(c.d.ti_sum, 0, sizeof(double) * (size_t)c.kp.R * c.kp.C, c.stream));
-  CK(cudaMemsetAsync(c.d.ti_n, 0, sizeof(long long), c.stream));
-  if ((st = evaluate_here(c))) return st;
-  return check_flags(c);
+  return set_states(c, r, 1, buf, nbytes);
 }
 
 cph_status cph_get_state_all(cph_ctx *ctx, void *buf, int64_t cap, int64_t *n) {
   if (!ctx || !n) return CPH_E_INVALID;
   Ctx &c = ctx->c;
-  int64_t one = 0;
-  cph_status st = cph_get_state(ctx, 0, nullptr, 0, &one);
-  if (st) return st;
-  *n = one * c.kp.R;
+  *n = (int64_t)(state_bytes(c) * c.kp.R);
   if (!buf) return CPH_OK;
   if (cap < *n) { c.err = "state buffer too small"; return CPH_E_INVALID; }
-  for (int r = 0; r < c.kp.R; ++r)
-    if ((st = cph_get_state(ctx, r, (char *)buf + (size_t)r * one, one, &one))) return st;
-  return CPH_OK;
+  cudaSetDevice(c.device);
+  cph_status st = cph_sync(ctx);
+  if (st) return st;
+  return get_states(c, 0, c.kp.R, buf);
 }
 
 cph_status cph_set_state_all(cph_ctx *ctx, const void *buf, int64_t nbytes) {
   if (!ctx || !buf) return CPH_E_INVALID;
   Ctx &c = ctx->c;
-  int64_t one = 0;
-  cph_status st = cph_get_state(ctx, 0, nullptr, 0, &one);
-  if (st || (st = cph_sync(ctx))) return st;
-  if (nbytes < one * c.kp.R) { c.err = "state blob too small"; return CPH_E_INVALID; }
-  for (int r = 0; r < c.kp.R; ++r)
-    if ((st = upload_state(c, r, (const char *)buf + (size_t)r * one, one))) return st;
-  // a new configuration: TI accumulators restart
-  CK(cudaMemsetAsync(c.d.ti_sum, 0, sizeof(double) * (size_t)c.kp.R * c.kp.C, c.stream));
-  CK(cudaMemsetAsync(c.d.ti_n, 0, sizeof(long long), c.stream));
-  if ((st = evaluate_here(c))) return st;
-  return check_flags(c);
+  cudaSetDevice(c.device);
+  cph_status st = cph_sync(ctx);
+  if (st) return st;
+  return set_states(c, 0, c.kp.R, buf, nbytes);
 }
 
 cph_status cph_profile_steps(cph_ctx *ctx, int64_t n_steps, double *ms, int64_t *launches) {
