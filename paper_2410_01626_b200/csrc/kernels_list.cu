@@ -2,8 +2,8 @@
 //
 // Every nstlist steps: atoms are binned into cells of edge >= rlist/2 (stencil +-2, or the
 // whole dimension when it has fewer than 5 cells), counting-sorted by cell, ordered by
-// original index inside each cell (deterministic layout), and all per-atom arrays are
-// permuted.  Then each atom gets a FULL neighbour list (both directions, so the pair kernel
+// (wrapped z, original index) inside each cell (deterministic layout), and all per-atom
+// arrays are permuted.  Then each atom gets a FULL neighbour list (both directions, so the pair kernel
 // needs no atomics) of the non-excluded atoms with float32 d^2 < rlist^2, evaluated with the
 // canonical round-to-nearest, no-contraction formula of DESIGN.md R14 so that the list is
 // bit-exact against the oracle's.  Entries: sorted slot (21 bits) | LJ type (5 bits) | image
@@ -94,9 +94,6 @@ __device__ __forceinline__ float rint_unit(float t) {
   return r;
 }
 
-// order each cell's atoms by (wrapped z, original index): a deterministic layout in which
-// 4 consecutive atoms of a cell form a compact z-slab "cluster" for the list prefilter
-// (insertion sort; cells hold ~20-60 atoms)
 // the canonical list decision for one pair (R14), used for fast-path candidates
 // inside the rounding band
 __device__ __forceinline__ bool canonical_in(float4 xj, float4 xi, float3 Lbox, float3 Linv, float rlist2) {
