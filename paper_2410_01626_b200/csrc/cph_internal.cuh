@@ -152,8 +152,9 @@ struct DboConfig {
 struct Ctx {
   KParams kp{};
   DevBufs d;
-  cudaStream_t stream = nullptr, stream_pme = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t stream = nullptr, stream_pme = nullptr, stream_nb = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork2 = nullptr, ev_join2 = nullptr;
+  bool prio = false;                                // pair kernel on a high-priority stream
   bool own_stream = false;
   cufftHandle plan_r2c = 0, plan_c2r = 0;
   void *(*dev_alloc)(size_t, void *) = nullptr;

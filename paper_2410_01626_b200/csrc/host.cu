@@ -229,7 +229,17 @@ int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
   cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid);
   k += launch_gather(c, sp);
   k += launch_hi_recip(c, sp);
-  k += launch_nonbonded(c, s, 1);
+  if (two_streams && c.prio) {
+    // the pair kernel on a high-priority stream: the PME chain (low priority) fills the SMs
+    // the pair kernel leaves free instead of displacing its CTAs
+    cudaEventRecord(c.ev_fork2, s);
+    cudaStreamWaitEvent(c.stream_nb, c.ev_fork2, 0);
+    k += launch_nonbonded(c, c.stream_nb, 1);
+    cudaEventRecord(c.ev_join2, c.stream_nb);
+    cudaStreamWaitEvent(s, c.ev_join2, 0);
+  } else {
+    k += launch_nonbonded(c, s, 1);
+  }
   if (two_streams) {
     cudaEventRecord(c.ev_join, c.stream_pme);
     cudaStreamWaitEvent(s, c.ev_join, 0);
@@ -292,7 +302,7 @@ cph_status capture_block(Ctx &c) {
   const bool two = getenv("CPH_ONE_STREAM") == nullptr;   // diagnostic switch: serialise NB and PME
   for (int s = 0; s < c.kp.nstlist; ++s) k += enqueue_step(c, s == c.kp.nstlist - 1, two);
   CK(cudaStreamEndCapture(c.stream, &g));
-  CK(cudaGraphInstantiate(&c.graph_block, g, 0));
+  CK(cudaGraphInstantiateWithFlags(&c.graph_block, g, c.prio ? cudaGraphInstantiateFlagUseNodePriority : 0));
   cudaGraphDestroy(g);
   c.graph_block_kernels = k;
   return CPH_OK;
@@ -639,7 +649,16 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     }
     c.own_stream = true;
   }
-  if (cudaStreamCreateWithFlags(&c.stream_pme, cudaStreamNonBlocking) != cudaSuccess ||
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  c.prio = getenv("CPH_NO_PRIO") == nullptr && prio_hi < prio_lo;
+  if (cudaStreamCreateWithPriority(&c.stream_nb, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c.ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c.ev_join2, cudaEventDisableTiming) != cudaSuccess) {
+    c.err = "stream/event creation failed";
+    return fail_create(ctx, CPH_E_CUDA);
+  }
+  if (cudaStreamCreateWithPriority(&c.stream_pme, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
       cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming) != cudaSuccess) {
     c.err = "stream/event creation failed";
@@ -870,6 +889,9 @@ void cph_destroy(cph_ctx *ctx) {
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
   if (c.ev_join) cudaEventDestroy(c.ev_join);
   if (c.stream_pme) cudaStreamDestroy(c.stream_pme);
+  if (c.stream_nb) cudaStreamDestroy(c.stream_nb);
+  if (c.ev_fork2) cudaEventDestroy(c.ev_fork2);
+  if (c.ev_join2) cudaEventDestroy(c.ev_join2);
   if (c.own_stream) cudaStreamDestroy(c.stream);
   delete ctx;
 }
