@@ -27,19 +27,19 @@ def test_his_micro_pka_from_bias_only_sampling(cph):
     s.state_q[:, 3] = s.state_q[:, 0]
     s.vmm[:] = 0.0
     levels = np.linspace(5.5, 8.0, 6)
-    per = 48
+    per = 128
     pH = np.repeat(levels, per)
     R = len(pH)
     rng = np.random.default_rng(17)
     w = np.stack([np.ones(R), 10 ** (pH - 6.53), 10 ** (pH - 6.92)], 1)
     st = np.array([rng.choice(3, p=wi / wi.sum()) for wi in w])
     lam0 = np.stack([np.zeros(R), (st > 0).astype(float), (st == 2).astype(float)], 1)
-    ctx = cph.cph_create(s, pH, replica_seeds(31, R), lambda0=lam0, barrier=2.0, nstout=20, frame_capacity=4096,
+    ctx = cph.cph_create(s, pH, replica_seeds(31, R), lambda0=lam0, barrier=2.0, nstout=20, frame_capacity=8192,
                          vel_replicas=np.stack([make_velocities(s, r) for r in range(R)]))
     ctx.cph_step(5000)
     for r in range(R):
         ctx.cph_get_frames(r)
-    ctx.cph_step(40000)
+    ctx.cph_step(60000)
     xd, xe = [], []
     for k in range(len(levels)):
         lp, lt = [], []

@@ -202,7 +202,7 @@ def test_gpu_sampling_follows_hh_when_coulomb_dvdl_vanishes(cph):
     s.state_q[:, 3] = s.state_q[:, 0]
     s.vmm[:] = 0.0
     levels = np.array([3.4, 4.4, 5.4, 6.5])
-    per = 128                          # replicas per pH: ~3 sigma margin at 0.03
+    per = 256                          # replicas per pH: standard error ~0.008 at pH = pKa
     pH = np.repeat(levels, per)
     R = len(pH)
     # start from the target populations (end states), so the run samples the stationary law
@@ -213,11 +213,11 @@ def test_gpu_sampling_follows_hh_when_coulomb_dvdl_vanishes(cph):
     lam0 = np.stack([(rng.random(R) < p_glu).astype(float), (his_state > 0).astype(float),
                      (his_state == 2).astype(float)], 1)
     ctx = cph.cph_create(s, pH, replica_seeds(7, R), lambda0=lam0, barrier=2.0, nstout=20,
-                         frame_capacity=2048, vel_replicas=np.stack([make_velocities(s, r) for r in range(R)]))
+                         frame_capacity=4096, vel_replicas=np.stack([make_velocities(s, r) for r in range(R)]))
     ctx.cph_step(5000)                 # equilibrate 10 ps
     for r in range(R):
         ctx.cph_get_frames(r)          # drop equilibration frames
-    ctx.cph_step(30000)                # 60 ps
+    ctx.cph_step(40000)                # 80 ps
     glu = np.zeros(len(levels))
     his_d = np.zeros(len(levels))
     his_e = np.zeros(len(levels))
