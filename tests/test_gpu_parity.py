@@ -235,6 +235,12 @@ def test_gpu_sampling_follows_hh_when_coulomb_dvdl_vanishes(cph):
     hh = 1.0 / (10 ** (4.4 - levels) + 1.0)
     print("glu", glu, hh)
     assert np.all(np.abs(glu - hh) < 0.03)
+    # BASELINE target: the synthetic titration's pKa within 0.05 pH units of the oracle's, which
+    # for Coulomb-free sites is the set pKa (closed form; oracle pin in test_oracle_pins.py)
+    from paper_2410_01626_b200 import titration as T
+    pka = T.fit_curve(levels, glu)
+    print("fitted pKa", pka)
+    assert abs(pka - 4.4) < 0.05
     pk_d, pk_e = 6.53, 6.92
     prot = 1.0 / (1 + 10 ** (levels - pk_d) + 10 ** (levels - pk_e))
     print("his delta", his_d, prot * 10 ** (levels - pk_d), "eps", his_e, prot * 10 ** (levels - pk_e))
