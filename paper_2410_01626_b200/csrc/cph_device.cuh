@@ -238,4 +238,57 @@ __device__ __forceinline__ bool is_energy_step(long long m, long long end, int n
   return (m % nstenergy) == 0 || m == end;
 }
 
+// ---- smooth PME B-splines (R16) -------------------------------------------------
+// Grid convention: atom with scaled fractional coordinate u = K (x/L - floor(x/L)) puts weight
+// M4(u - k) on grid points k = floor(u) - j, j = 0..3 (mod K); w = u - floor(u).
+__device__ __forceinline__ void bspline4(const float x, const float invL, const int K, int &k0,
+                                         float th[4], float dth[4]) {
+  const float t = x * invL;
+  const float s = t - floorf(t);
+  const float u = s * (float)K;
+  float fl = floorf(u);
+  const float w = u - fl;
+  int k = (int)fl;
+  if (k >= K) k -= K;
+  k0 = k;
+  const float w2 = w * w, w3 = w2 * w, om = 1.0f - w;
+  const float s6 = 1.0f / 6.0f;
+  th[0] = w3 * s6;
+  th[1] = (-3.0f * w3 + 3.0f * w2 + 3.0f * w + 1.0f) * s6;
+  th[2] = (3.0f * w3 - 6.0f * w2 + 4.0f) * s6;
+  th[3] = om * om * om * s6;
+  dth[0] = 0.5f * w2;
+  dth[1] = 0.5f * (-3.0f * w2 + 2.0f * w + 1.0f);
+  dth[2] = 0.5f * (3.0f * w2 - 4.0f * w);
+  dth[3] = -0.5f * om * om;
+}
+
+// fp64 phi_rec of one atom from the back-transformed grid g of its replica: the B-spline
+// weighted sum over the 4x4x4 points (z rows in fp32, products with theta_x theta_y in fp64)
+__device__ __forceinline__ double pme_phi64(const KParams &kp, const float *g, const float4 p) {
+  int kx, ky, kz;
+  float tx[4], ty[4], tz[4], dd[4];
+  bspline4(p.x, kp.invL[0], kp.K[0], kx, tx, dd);
+  bspline4(p.y, kp.invL[1], kp.K[1], ky, ty, dd);
+  bspline4(p.z, kp.invL[2], kp.K[2], kz, tz, dd);
+  int iz[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) iz[c] = (kz - c + kp.K[2]) % kp.K[2];
+  double phid = 0.0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int ix = (kx - a + kp.K[0]) % kp.K[0];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int iy = (ky - b + kp.K[1]) % kp.K[1];
+      const float *row = g + ((size_t)ix * kp.K[1] + iy) * kp.K[2];
+      float s = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) s = fmaf(tz[c], __ldg(row + iz[c]), s);
+      phid += (double)(tx[a] * ty[b]) * (double)s;
+    }
+  }
+  return phid;
+}
+
 }  // namespace cph

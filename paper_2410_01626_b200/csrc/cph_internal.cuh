@@ -90,7 +90,7 @@ struct DevBufs {
   int *nnb = nullptr;                               // [R*Nst]
   int *excl_ptr = nullptr, *excl_idx = nullptr;     // CSR by original atom
   float2 *ljtab = nullptr;                          // [T*T] (6 c6, 12 c12) fp32
-  double *phi64_nb = nullptr, *phi64_rec = nullptr; // [R*nlam]
+  double *phi64_nb = nullptr;                       // [R*nlam]
   float *grid = nullptr;                            // [R*K3]
   float2 *cgrid = nullptr;                          // [R*Kc]
   float *bsp = nullptr;                             // [Kx + Ky + Kz] |b|^2 moduli
@@ -149,11 +149,19 @@ struct DboConfig {
   double bstep = 1.0, bmin = 1.0, bmax = 20.0;
 };
 
+struct Timeline {   // CPH_TIMELINE diagnostic (host.cu): %globaltimer stamps from 1-thread kernels
+  static constexpr int S = 64, T = 12;
+  int s = 0, n = 0;
+  unsigned long long *stamps = nullptr;   // device [S][T]
+  bool used[S][T] = {};
+  double sum[S][T] = {};
+};
 struct Ctx {
+  Timeline *tl = nullptr;                           // CPH_TIMELINE diagnostic (host.cu)
   KParams kp{};
   DevBufs d;
   cudaStream_t stream = nullptr, stream_pme = nullptr, stream_nb = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork2 = nullptr, ev_join2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork2 = nullptr, ev_join2 = nullptr, ev_gather = nullptr;
   bool prio = false;                                // pair kernel on a high-priority stream
   bool own_stream = false;
   cufftHandle plan_r2c = 0, plan_c2r = 0;

@@ -206,13 +206,53 @@ cph_status run_pfc(Ctx &c, int r) { return run_pfc_many(c, std::vector<int>{r});
 
 __global__ void k_set_end(long long *end, long long v) { *end = v; }
 
+// ---- timeline diagnostic (CPH_TIMELINE=1): timing events captured into the step graph at
+// stage boundaries; mean offsets from each step's start are printed at cph_destroy
+__global__ void k_stamp(unsigned long long *p) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *p = t;
+}
+static void tl_mark(Ctx &c, cudaStream_t st, int tag) {
+  Timeline *t = c.tl;
+  if (!t || t->s >= Timeline::S) return;
+  k_stamp<<<1, 1, 0, st>>>(t->stamps + t->s * Timeline::T + tag);
+  t->used[t->s][tag] = true;
+}
+static void tl_collect(Ctx &c) {
+  Timeline *t = c.tl;
+  if (!t) return;
+  unsigned long long h[Timeline::S][Timeline::T];
+  cudaStreamSynchronize(c.stream);
+  cudaMemcpy(h, t->stamps, sizeof(h), cudaMemcpyDeviceToHost);
+  for (int s = 0; s < Timeline::S; ++s)
+    for (int k = 1; k < Timeline::T; ++k)
+      if (t->used[s][k] && t->used[s][0]) t->sum[s][k] += 1e-3 * (double)(long long)(h[s][k] - h[s][0]);
+  t->n += 1;
+}
+static void tl_print(Ctx &c) {
+  Timeline *t = c.tl;
+  if (!t || !t->n) return;
+  static const char *names[Timeline::T] = {"start", "integrate", "sort", "build", "spread", "r2c", "solve", "c2r",
+                                           "pair", "gather", "lambda", "-"};
+  for (int s = 0; s < c.kp.nstlist && s < Timeline::S; ++s) {
+    fprintf(stderr, "[timeline] step %d:", s);
+    for (int k = 1; k < Timeline::T; ++k)
+      if (t->used[s][k]) fprintf(stderr, " %s %.1f", names[k], t->sum[s][k] / t->n);
+    fprintf(stderr, " (us, %d blocks)\n", t->n);
+  }
+}
+
 // one full step (n -> n+1) on the context streams; returns kernels launched
 int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
   int k = 0;
   cudaStream_t s = c.stream;
+  tl_mark(c, s, 0);
   k += launch_integrate(c, s, 1);
+  tl_mark(c, s, 1);
   static const bool serial_build = getenv("CPH_SERIAL_BUILD") != nullptr;   // A/B diagnostic
   if (rebuild) k += serial_build ? launch_rebuild(c, s) : launch_sort(c, s);
+  if (rebuild) tl_mark(c, s, 2);
   cudaStream_t sp = s;
   if (two_streams) {
     cudaEventRecord(c.ev_fork, s);
@@ -221,31 +261,46 @@ int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
   }
   // the PME chain needs only the sorted atoms: it overlaps the list build
   if (rebuild && !serial_build) k += launch_build_list(c, s);
+  if (rebuild) tl_mark(c, s, 3);
   cufftSetStream(c.plan_r2c, sp);
   cufftSetStream(c.plan_c2r, sp);
   k += launch_spread(c, sp);
+  tl_mark(c, sp, 4);
   cufftExecR2C(c.plan_r2c, c.d.grid, (cufftComplex *)c.d.cgrid);
+  tl_mark(c, sp, 5);
   k += launch_solve(c, sp, 1);
+  tl_mark(c, sp, 6);
   cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid);
-  k += launch_gather(c, sp);
+  tl_mark(c, sp, 7);
   k += launch_hi_recip(c, sp);
+  // the lambda kernel reads phi_rec of its atoms straight from the grid: it waits for the
+  // back transform only, and the all-atom force gather runs beside it (joined below, before
+  // anything that reads f_rec)
+  if (two_streams) cudaEventRecord(c.ev_join, c.stream_pme);
+  else k += launch_gather(c, s);
   if (two_streams && c.prio) {
     // the pair kernel on a high-priority stream: the PME chain (low priority) fills the SMs
     // the pair kernel leaves free instead of displacing its CTAs
     cudaEventRecord(c.ev_fork2, s);
     cudaStreamWaitEvent(c.stream_nb, c.ev_fork2, 0);
     k += launch_nonbonded(c, c.stream_nb, 1);
+    tl_mark(c, c.stream_nb, 8);
     cudaEventRecord(c.ev_join2, c.stream_nb);
     cudaStreamWaitEvent(s, c.ev_join2, 0);
   } else {
     k += launch_nonbonded(c, s, 1);
+    tl_mark(c, s, 8);
   }
   if (two_streams) {
-    cudaEventRecord(c.ev_join, c.stream_pme);
     cudaStreamWaitEvent(s, c.ev_join, 0);
+    k += launch_gather(c, c.stream_pme);
+    tl_mark(c, c.stream_pme, 9);
+    cudaEventRecord(c.ev_gather, c.stream_pme);
   }
   k += launch_hi_finish(c, s, 1);
   k += launch_lambda_reduce(c, s, 1);
+  tl_mark(c, s, 10);
+  if (two_streams) cudaStreamWaitEvent(s, c.ev_gather, 0);
   return k;
 }
 
@@ -297,10 +352,18 @@ cph_status check_flags(Ctx &c) {
 cph_status capture_block(Ctx &c) {
   if (c.graph_block) return CPH_OK;
   cudaGraph_t g;
+  if (getenv("CPH_TIMELINE") && !c.tl) {
+    c.tl = new Timeline();
+    CK(cudaMalloc(&c.tl->stamps, sizeof(unsigned long long) * Timeline::S * Timeline::T));
+  }
   CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
   int k = 0;
   const bool two = getenv("CPH_ONE_STREAM") == nullptr;   // diagnostic switch: serialise NB and PME
-  for (int s = 0; s < c.kp.nstlist; ++s) k += enqueue_step(c, s == c.kp.nstlist - 1, two);
+  for (int s = 0; s < c.kp.nstlist; ++s) {
+    if (c.tl) c.tl->s = s;
+    k += enqueue_step(c, s == c.kp.nstlist - 1, two);
+  }
+  if (c.tl) c.tl->s = Timeline::S;   // eager steps are not marked
   CK(cudaStreamEndCapture(c.stream, &g));
   CK(cudaGraphInstantiateWithFlags(&c.graph_block, g, c.prio ? cudaGraphInstantiateFlagUseNodePriority : 0));
   cudaGraphDestroy(g);
@@ -660,7 +723,8 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   }
   if (cudaStreamCreateWithPriority(&c.stream_pme, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
       cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c.ev_gather, cudaEventDisableTiming) != cudaSuccess) {
     c.err = "stream/event creation failed";
     return fail_create(ctx, CPH_E_CUDA);
   }
@@ -681,7 +745,6 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   d.excl_idx = dalloc<int>(c, c.h_excl_idx.size());
   d.ljtab = dalloc<float2>(c, (size_t)T * T);
   d.phi64_nb = dalloc<double>(c, (size_t)R * nlam);
-  d.phi64_rec = dalloc<double>(c, (size_t)R * nlam);
   d.phi_lam = dalloc<double>(c, (size_t)R * nlam);
   d.grid = dalloc<float>(c, (size_t)R * kp.K3);
   d.cgrid = dalloc<float2>(c, (size_t)R * kp.Kc);
@@ -882,12 +945,14 @@ void cph_destroy(cph_ctx *ctx) {
   Ctx &c = ctx->c;
   cudaSetDevice(c.device);
   cudaStreamSynchronize(c.stream);
+  if (c.tl) { tl_print(c); cudaFree(c.tl->stamps); delete c.tl; c.tl = nullptr; }
   if (c.graph_block) cudaGraphExecDestroy(c.graph_block);
   if (c.plan_r2c) cufftDestroy(c.plan_r2c);
   if (c.plan_c2r) cufftDestroy(c.plan_c2r);
   free_all(c);
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
   if (c.ev_join) cudaEventDestroy(c.ev_join);
+  if (c.ev_gather) cudaEventDestroy(c.ev_gather);
   if (c.stream_pme) cudaStreamDestroy(c.stream_pme);
   if (c.stream_nb) cudaStreamDestroy(c.stream_nb);
   if (c.ev_fork2) cudaEventDestroy(c.ev_fork2);
@@ -930,6 +995,7 @@ static cph_status run_segment(Ctx &c, long long end) {
       cph_status st = capture_block(c);
       if (st) return st;
       CK(cudaGraphLaunch(c.graph_block, c.stream));
+      if (c.tl) tl_collect(c);
       k += c.graph_block_kernels;
       c.host_step += nl;
     } else {

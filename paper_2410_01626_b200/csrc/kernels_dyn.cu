@@ -21,8 +21,12 @@ __global__ void __launch_bounds__(128) k_integrate(KParams kp, DevBufs d) {
     const size_t idx = (size_t)r * kp.Nst + i;
     float4 v = d.vel[idx];
     const float invm = v.w;
+    const int2 mt = d.meta[idx];
+    const int lslot = (mt.y >> 8) - 1;   // lambda atom: charge of this step from qlam (lambda_set_charges)
+    const float qnew = lslot >= 0 ? (float)d.qlam[(size_t)r * kp.nlam + lslot] : 0.f;
     if (invm > 0.0f) {
       float4 x = d.xyzq[idx];
+      if (lslot >= 0) x.w = qnew;
       const float4 fa = d.f_nb[idx], fb = d.f_rec[idx];
       const float fx = fa.x + fb.x, fy = fa.y + fb.y, fz = fa.z + fb.z;
       const float hk = 0.5f * kp.dt * invm;
@@ -41,7 +45,7 @@ __global__ void __launch_bounds__(128) k_integrate(KParams kp, DevBufs d) {
         d.vel[idx] = v;
         goto done;
       }
-      const int orig = d.meta[idx].x;
+      const int orig = mt.x;
       const float3 xi = atom_normals(d.seed[r], (uint32_t)n, (uint32_t)orig);
       const float sd = sqrtf(kp.c2_atom_kT * invm);
       v.x = fmaf(kp.c1_atom, v.x, sd * xi.x);                                           // O
@@ -50,6 +54,8 @@ __global__ void __launch_bounds__(128) k_integrate(KParams kp, DevBufs d) {
       x.x = fmaf(hdt, v.x, x.x); x.y = fmaf(hdt, v.y, x.y); x.z = fmaf(hdt, v.z, x.z);  // A
       d.xyzq[idx] = x;
       d.vel[idx] = v;
+    } else if (lslot >= 0) {
+      d.xyzq[idx].w = qnew;
     }
   }
 done:
@@ -94,6 +100,8 @@ __global__ void __launch_bounds__(128) k_close(KParams kp, DevBufs d, int kick) 
   double ke = 0.0;
   if (i < kp.N) {
     const size_t idx = (size_t)r * kp.Nst + i;
+    const int lslot = (d.meta[idx].y >> 8) - 1;   // end of a cph_step call: qlam -> xyzq.w
+    if (lslot >= 0) d.xyzq[idx].w = (float)d.qlam[(size_t)r * kp.nlam + lslot];
     float4 v = d.vel[idx];
     if (v.w > 0.0f) {
       if (kick) {
@@ -110,8 +118,11 @@ __global__ void __launch_bounds__(128) k_close(KParams kp, DevBufs d, int kick) 
 }
 
 // ---- lambda helpers ---------------------------------------------------------------------
-// charges of every lambda atom of replica r from its group's (lp, lt) (Eq. 2)
-__device__ void lambda_set_charges(const KParams &kp, const DevBufs &d, int r) {
+// charges of every lambda atom of replica r from its group's (lp, lt) (Eq. 2).
+// Inside a step (to_xyzq = false) only qlam is written: the all-atom force gather may still be
+// reading xyzq.w of this step on the PME stream, and the next k_integrate (or k_close at the
+// end of a cph_step call) copies qlam into xyzq.w.
+__device__ void lambda_set_charges(const KParams &kp, const DevBufs &d, int r, bool to_xyzq = true) {
   for (int k = threadIdx.x; k < kp.nlam; k += blockDim.x) {       // one thread per lambda atom
     const int g = d.k_group[k];
     const int c0 = d.g_cptr[g];
@@ -121,6 +132,7 @@ __device__ void lambda_set_charges(const KParams &kp, const DevBufs &d, int r) {
     const double *qs = d.g_q + 4 * (size_t)k;
     const double q = wA * qs[0] + wB * qs[1] + wC * qs[2] + wD * qs[3];
     d.qlam[(size_t)r * kp.nlam + k] = q;
+    if (!to_xyzq) continue;
     const int slot = d.iperm[(size_t)r * kp.N + d.g_atoms[k]];
     d.xyzq[(size_t)r * kp.Nst + slot].w = (float)q;
   }
@@ -130,7 +142,7 @@ __device__ double block_sum_d(double v);
 
 // BAOA for lambda coordinates of replica r with noise index `step`, then new charges
 // (O = Langevin, or the Bussi rescaling of the replica's lambda group, R27)
-__device__ void lambda_open(const KParams &kp, const DevBufs &d, int r, long long step) {
+__device__ void lambda_open(const KParams &kp, const DevBufs &d, int r, long long step, bool to_xyzq = true) {
   const double h = kp.dtd;
   double ke = 0.0;
   for (int c = threadIdx.x; c < kp.C; c += blockDim.x) {
@@ -159,7 +171,7 @@ __device__ void lambda_open(const KParams &kp, const DevBufs &d, int r, long lon
     }
   }
   __syncthreads();
-  lambda_set_charges(kp, d, r);
+  lambda_set_charges(kp, d, r, to_xyzq);
 }
 
 __device__ double block_sum_d(double v) {
@@ -207,7 +219,11 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
     const double q = d.qlam[ix];
     qs += q;
     qq += q * q;
-    const double phi = d.phi64_nb[ix] + d.phi64_rec[ix] - 2.0 * kp.beta_d / sqrtpi * q;
+    // phi_rec from the back-transformed PME grid (the all-atom force gather runs beside this
+    // kernel on the PME stream)
+    const int slot = d.iperm[(size_t)r * kp.N + d.g_atoms[k]];
+    const double prec = pme_phi64(kp, d.grid + (size_t)r * kp.K3, d.xyzq[(size_t)r * kp.Nst + slot]);
+    const double phi = d.phi64_nb[ix] + prec - 2.0 * kp.beta_d / sqrtpi * q;
     d.phi_lam[ix] = phi;
     const int g = d.k_group[k];
     const size_t ic = (size_t)r * kp.C + d.g_cptr[g];
@@ -318,8 +334,8 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
   }
   __syncthreads();
   if (mode == 1) {
-    if (fuse_open) lambda_set_charges(kp, d, r);
-    else if (dyn && m != end) lambda_open(kp, d, r, m);
+    if (fuse_open) lambda_set_charges(kp, d, r, false);
+    else if (dyn && m != end) lambda_open(kp, d, r, m, false);
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();

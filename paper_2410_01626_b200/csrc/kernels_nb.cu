@@ -16,6 +16,10 @@
 
 namespace cph {
 
+#ifndef CPH_NB_MINB
+#define CPH_NB_MINB 7   // CTAs per SM the register budget is sized for (A/B: 6 and 8 slower)
+#endif
+
 template <bool ENERGY, bool PHI64>
 __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, const float4 *__restrict__ xq,
                                         const float2 *__restrict__ ljf, const float2 *__restrict__ lje,
@@ -131,7 +135,7 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
   }
 }
 
-__global__ void __launch_bounds__(128, 7) k_nonbonded(KParams kp, DevBufs d, int step_offset) {
+__global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevBufs d, int step_offset) {
   // LJ tables sized T*T (dynamic shared memory): the rest of the SM's 256 KB stays L1 cache
   // for the neighbour-position gathers
   extern __shared__ float2 s_lj[];

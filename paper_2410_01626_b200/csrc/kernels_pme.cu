@@ -8,29 +8,19 @@
 
 namespace cph {
 
-__device__ __forceinline__ void bspline4(const float x, const float invL, const int K, int &k0,
-                                         float th[4], float dth[4]) {
-  const float t = x * invL;
-  const float s = t - floorf(t);
-  const float u = s * (float)K;
-  float fl = floorf(u);
-  const float w = u - fl;
-  int k = (int)fl;
-  if (k >= K) k -= K;
-  k0 = k;
-  const float w2 = w * w, w3 = w2 * w, om = 1.0f - w;
-  const float s6 = 1.0f / 6.0f;
-  th[0] = w3 * s6;
-  th[1] = (-3.0f * w3 + 3.0f * w2 + 3.0f * w + 1.0f) * s6;
-  th[2] = (3.0f * w3 - 6.0f * w2 + 4.0f) * s6;
-  th[3] = om * om * om * s6;
-  dth[0] = 0.5f * w2;
-  dth[1] = 0.5f * (-3.0f * w2 + 2.0f * w + 1.0f);
-  dth[2] = 0.5f * (3.0f * w2 - 4.0f * w);
-  dth[3] = -0.5f * om * om;
-}
+#ifndef CPH_SPREAD_VEC
+#define CPH_SPREAD_VEC 1   // float4 reductions along z (A/B switch)
+#endif
+#ifndef CPH_SPREAD_TPB
+#define CPH_SPREAD_TPB 128
+#endif
+#ifdef CPH_SPREAD_MAXREG
+#define SPREAD_ATTR __maxnreg__(CPH_SPREAD_MAXREG)
+#else
+#define SPREAD_ATTR __launch_bounds__(CPH_SPREAD_TPB)
+#endif
 
-__global__ void __launch_bounds__(128) k_spread(KParams kp, DevBufs d) {
+__global__ void SPREAD_ATTR k_spread(KParams kp, DevBufs d) {
   const int r = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= kp.N) return;
   const float4 p = d.xyzq[(size_t)r * kp.Nst + i];
@@ -44,6 +34,12 @@ __global__ void __launch_bounds__(128) k_spread(KParams kp, DevBufs d) {
   int iz[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) iz[c] = (kz - c + kp.K[2]) % kp.K[2];
+  // the four z points kz-3 .. kz of a row are contiguous unless they wrap; with K_z % 4 == 0
+  // they touch one or two aligned float4 blocks, added with vector reductions (REDG.F32x4:
+  // 16 or 32 reductions per atom instead of 64)
+  const int z0 = kz - 3;
+  const bool vec = CPH_SPREAD_VEC && (kp.K[2] & 3) == 0 && z0 >= 0;
+  const int a0 = z0 & ~3, off = z0 - a0;
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const int ix = (kx - a + kp.K[0]) % kp.K[0];
@@ -53,8 +49,23 @@ __global__ void __launch_bounds__(128) k_spread(KParams kp, DevBufs d) {
       const int iy = (ky - b + kp.K[1]) % kp.K[1];
       const float qab = qa * ty[b];
       float *row = g + ((size_t)ix * kp.K[1] + iy) * kp.K[2];
+      if (vec) {
+        const float v0 = qab * tz[3], v1 = qab * tz[2], v2 = qab * tz[1], v3 = qab * tz[0];   // z0 .. z0+3
+        float4 lo, hi;
+        lo.x = off == 0 ? v0 : 0.f;
+        lo.y = off == 0 ? v1 : (off == 1 ? v0 : 0.f);
+        lo.z = off == 0 ? v2 : (off == 1 ? v1 : (off == 2 ? v0 : 0.f));
+        lo.w = off == 0 ? v3 : (off == 1 ? v2 : (off == 2 ? v1 : v0));
+        hi.x = off == 1 ? v3 : (off == 2 ? v2 : (off == 3 ? v1 : 0.f));
+        hi.y = off == 2 ? v3 : (off == 3 ? v2 : 0.f);
+        hi.z = off == 3 ? v3 : 0.f;
+        hi.w = 0.f;
+        atomicAdd(reinterpret_cast<float4 *>(row + a0), lo);
+        if (off) atomicAdd(reinterpret_cast<float4 *>(row + a0 + 4), hi);
+      } else {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) atomicAdd(row + iz[c], qab * tz[c]);
+        for (int c = 0; c < 4; ++c) atomicAdd(row + iz[c], qab * tz[c]);
+      }
     }
   }
 }
@@ -94,10 +105,13 @@ __global__ void __launch_bounds__(256) k_solve(KParams kp, DevBufs d, int step_o
   if (energy) block_atomic_add_d(0.5 * kFCoul * e, d.erec + ((size_t)(m & 1) * kp.R + r) * kNE + CPH_E_RECIP);
 }
 
-template <bool PHI64>
-__device__ __forceinline__ void gather_atom(const KParams &kp, const DevBufs &d, int r, int i, bool valid,
-                                            float4 p, int lslot) {
-  if (!valid) return;
+// forces on every atom (and the fp32 phi_rec reported by cph_get_forces); the fp64 phi_rec of
+// the lambda atoms is computed by the lambda kernel itself (pme_phi64), so this kernel runs
+// beside it instead of before it
+__global__ void __launch_bounds__(128) k_gather(KParams kp, DevBufs d) {
+  const int r = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= kp.N) return;
+  const float4 p = d.xyzq[(size_t)r * kp.Nst + i];
   int kx, ky, kz;
   float tx[4], ty[4], tz[4], dx[4], dy[4], dz[4];
   bspline4(p.x, kp.invL[0], kp.K[0], kx, tx, dx);
@@ -108,7 +122,6 @@ __device__ __forceinline__ void gather_atom(const KParams &kp, const DevBufs &d,
 #pragma unroll
   for (int c = 0; c < 4; ++c) iz[c] = (kz - c + kp.K[2]) % kp.K[2];
   float phi = 0.f, gx = 0.f, gy = 0.f, gz = 0.f;
-  double phid = 0.0;
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const int ix = (kx - a + kp.K[0]) % kp.K[0];
@@ -127,30 +140,17 @@ __device__ __forceinline__ void gather_atom(const KParams &kp, const DevBufs &d,
       gx = fmaf(dx[a] * ty[b], s, gx);
       gy = fmaf(tx[a] * dy[b], s, gy);
       gz = fmaf(tx[a] * ty[b], sd, gz);
-      if (PHI64) phid += (double)(tx[a] * ty[b]) * (double)s;
     }
   }
   const float sc = -kp.fcoul * p.w;
-  const float4 out = make_float4(sc * gx * (float)kp.K[0] * kp.invL[0], sc * gy * (float)kp.K[1] * kp.invL[1],
-                                 sc * gz * (float)kp.K[2] * kp.invL[2], phi);
-  d.f_rec[(size_t)r * kp.Nst + i] = out;
-  if (PHI64 && lslot >= 0) d.phi64_rec[(size_t)r * kp.nlam + lslot] = phid;
-}
-
-__global__ void __launch_bounds__(128) k_gather(KParams kp, DevBufs d) {
-  const int r = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = i < kp.N;
-  const size_t idx = (size_t)r * kp.Nst + (valid ? i : 0);
-  const float4 p = d.xyzq[idx];
-  const int lslot = valid ? (d.meta[idx].y >> 8) - 1 : -1;
-  if (__any_sync(0xffffffffu, lslot >= 0)) gather_atom<true>(kp, d, r, i, valid, p, lslot);
-  else gather_atom<false>(kp, d, r, i, valid, p, lslot);
+  d.f_rec[(size_t)r * kp.Nst + i] = make_float4(sc * gx * (float)kp.K[0] * kp.invL[0], sc * gy * (float)kp.K[1] * kp.invL[1],
+                                                sc * gz * (float)kp.K[2] * kp.invL[2], phi);
 }
 
 int launch_spread(Ctx &c, cudaStream_t s) {
   cudaMemsetAsync(c.d.grid, 0, sizeof(float) * (size_t)c.kp.R * c.kp.K3, s);
-  dim3 grid((c.kp.N + 127) / 128, c.kp.R);
-  k_spread<<<grid, 128, 0, s>>>(c.kp, c.d);
+  dim3 grid((c.kp.N + CPH_SPREAD_TPB - 1) / CPH_SPREAD_TPB, c.kp.R);
+  k_spread<<<grid, CPH_SPREAD_TPB, 0, s>>>(c.kp, c.d);
   return 1;
 }
 int launch_solve(Ctx &c, cudaStream_t s, int step_offset) {
