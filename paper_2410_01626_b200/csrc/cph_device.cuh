@@ -264,31 +264,33 @@ __device__ __forceinline__ void bspline4(const float x, const float invL, const 
 }
 
 // fp64 phi_rec of one atom from the back-transformed grid g of its replica: the B-spline
-// weighted sum over the 4x4x4 points (z rows in fp32, products with theta_x theta_y in fp64)
-__device__ __forceinline__ double pme_phi64(const KParams &kp, const float *g, const float4 p) {
-  int kx, ky, kz;
-  float tx[4], ty[4], tz[4], dd[4];
-  bspline4(p.x, kp.invL[0], kp.K[0], kx, tx, dd);
-  bspline4(p.y, kp.invL[1], kp.K[1], ky, ty, dd);
-  bspline4(p.z, kp.invL[2], kp.K[2], kz, tz, dd);
-  int iz[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) iz[c] = (kz - c + kp.K[2]) % kp.K[2];
-  double phid = 0.0;
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
+// weighted sum over the 4x4x4 points (z rows in fp32, products with theta_x theta_y in fp64),
+// spread over 16 lanes (one (x, y) row of 4 z points each, aligned 16-lane
+// groups) and reduced with a fixed shuffle tree; every lane of the group returns the total.
+// All 32 lanes of the warp must call it (inactive groups pass act = false).
+__device__ __forceinline__ double pme_phi64_x16(const KParams &kp, const float *g, const float4 p, bool act) {
+  const int ab = threadIdx.x & 15, a = ab >> 2, b = ab & 3;
+  double v = 0.0;
+  if (act) {
+    int kx, ky, kz;
+    float tx[4], ty[4], tz[4], dd[4];
+    bspline4(p.x, kp.invL[0], kp.K[0], kx, tx, dd);
+    bspline4(p.y, kp.invL[1], kp.K[1], ky, ty, dd);
+    bspline4(p.z, kp.invL[2], kp.K[2], kz, tz, dd);
     const int ix = (kx - a + kp.K[0]) % kp.K[0];
+    const int iy = (ky - b + kp.K[1]) % kp.K[1];
+    const float *row = g + ((size_t)ix * kp.K[1] + iy) * kp.K[2];
+    float sa = 0.f;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int iy = (ky - b + kp.K[1]) % kp.K[1];
-      const float *row = g + ((size_t)ix * kp.K[1] + iy) * kp.K[2];
-      float s = 0.f;
+    for (int c = 0; c < 4; ++c) sa = fmaf(tz[c], __ldg(row + (kz - c + kp.K[2]) % kp.K[2]), sa);
+    float txa = tx[0], tyb = ty[0];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) s = fmaf(tz[c], __ldg(row + iz[c]), s);
-      phid += (double)(tx[a] * ty[b]) * (double)s;
-    }
+    for (int q = 1; q < 4; ++q) { txa = a == q ? tx[q] : txa; tyb = b == q ? ty[q] : tyb; }
+    v = (double)(txa * tyb) * (double)sa;
   }
-  return phid;
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
 }  // namespace cph

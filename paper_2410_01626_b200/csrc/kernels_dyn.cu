@@ -212,17 +212,26 @@ __global__ void __launch_bounds__(256) k_lambda_reduce(KParams kp, DevBufs d, in
   // net-charge term -pi Q/(V beta^2) is the same for every atom and every group's charge is
   // constant in lambda (sum_i dq_i/dlambda = 0, checked at create), so it adds nothing to
   // dV/dlambda; it enters the energies and cph_get_forces' phi only.
-  extern __shared__ double s_dq[];            // [2 * nlam]
+  extern __shared__ double s_dq[];            // [3 * nlam]: 2 products per atom, then phi_rec
+  double *s_prec = s_dq + 2 * kp.nlam;
+  // phi_rec of the lambda atoms from the back-transformed PME grid, 16 lanes per atom (the
+  // all-atom force gather runs beside this kernel on the PME stream)
+  for (int w0 = 0; w0 < 16 * kp.nlam; w0 += blockDim.x) {
+    const int w = w0 + threadIdx.x, k = w >> 4;
+    const bool act = k < kp.nlam;
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (act) p = d.xyzq[(size_t)r * kp.Nst + d.iperm[(size_t)r * kp.N + d.g_atoms[k]]];
+    const double v = pme_phi64_x16(kp, d.grid + (size_t)r * kp.K3, p, act);
+    if (act && (w & 15) == 0) s_prec[k] = v;
+  }
+  __syncthreads();
   double qs = 0.0, qq = 0.0;                  // total lambda charge and sum of squares
   for (int k = threadIdx.x; k < kp.nlam; k += blockDim.x) {
     const size_t ix = (size_t)r * kp.nlam + k;
     const double q = d.qlam[ix];
     qs += q;
     qq += q * q;
-    // phi_rec from the back-transformed PME grid (the all-atom force gather runs beside this
-    // kernel on the PME stream)
-    const int slot = d.iperm[(size_t)r * kp.N + d.g_atoms[k]];
-    const double prec = pme_phi64(kp, d.grid + (size_t)r * kp.K3, d.xyzq[(size_t)r * kp.Nst + slot]);
+    const double prec = s_prec[k];
     const double phi = d.phi64_nb[ix] + prec - 2.0 * kp.beta_d / sqrtpi * q;
     d.phi_lam[ix] = phi;
     const int g = d.k_group[k];
@@ -374,13 +383,13 @@ int launch_close(Ctx &c, cudaStream_t s, int kick) {
   return 1;
 }
 int launch_lambda_reduce(Ctx &c, cudaStream_t s, int mode) {
-  const size_t smem = 2 * sizeof(double) * (size_t)c.kp.nlam;
+  const size_t smem = 3 * sizeof(double) * (size_t)c.kp.nlam;
   static size_t configured = 48 * 1024;
   if (smem > configured) {
     cudaFuncSetAttribute(k_lambda_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = smem;
   }
-  k_lambda_reduce<<<c.kp.R, 256, 2 * sizeof(double) * (size_t)c.kp.nlam, s>>>(c.kp, c.d, mode);
+  k_lambda_reduce<<<c.kp.R, 256, smem, s>>>(c.kp, c.d, mode);
   return 1;
 }
 int launch_lambda_open(Ctx &c, cudaStream_t s) {
