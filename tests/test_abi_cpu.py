@@ -11,8 +11,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def cph():
-    from paper_2410_01626_b200 import build
-    build.build()
+    import __graft_entry__
+    __graft_entry__.build()
     import paper_2410_01626_b200 as m
     return m
 
