@@ -714,7 +714,10 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   }
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  c.prio = getenv("CPH_NO_PRIO") == nullptr && prio_hi < prio_lo;
+  c.prio = getenv("CPH_NO_PRIO") == nullptr && prio_hi != prio_lo;
+  // A/B diagnostic: CPH_PRIO_SWAP=1 puts the PME chain on the high-priority stream instead
+  static const bool swap = getenv("CPH_PRIO_SWAP") != nullptr;
+  if (swap) std::swap(prio_lo, prio_hi);
   if (cudaStreamCreateWithPriority(&c.stream_nb, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreateWithFlags(&c.ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c.ev_join2, cudaEventDisableTiming) != cudaSuccess) {
