@@ -120,7 +120,7 @@ class CphError(RuntimeError):
 def load_library(path: str = LIB_PATH):
     """Load libcph.so and declare every exported symbol; raises if anything is missing."""
     if not os.path.exists(path):
-        raise ImportError(f"{path} not built: run `python -m paper_2410_01626_b200.build` "
+        raise ImportError(f"{path} not built: run `python -c \"import __graft_entry__ as g; g.build()\"` "
                           "(there is no CPU fallback)")
     lib = C.CDLL(path)
     for name, (res, args) in EXPORTS.items():
