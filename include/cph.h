@@ -220,8 +220,12 @@ int32_t cph_n_coords(const cph_ctx *ctx);
 int32_t cph_n_atoms(const cph_ctx *ctx);
 int32_t cph_n_replicas(const cph_ctx *ctx);
 
-/* Change one replica's pH: recomputes the PFC well depths (host) and uploads
- * them; takes effect at the next step.  replica in [0, R). */
+/* The CUDA stream every call of this context enqueues on (the cph_params.cuda_stream the
+ * caller passed, or the context's own non-blocking stream when that was NULL). */
+void *cph_get_stream(const cph_ctx *ctx);
+/* Change one replica's pH: recomputes the PFC well depths (host), uploads them and
+ * re-evaluates dV_bias/dlambda and E_bias at the current lambda (the next half kick and
+ * the getters see the new pH).  replica in [0, R). */
 cph_status cph_set_pH(cph_ctx *ctx, int32_t replica, double pH);
 
 /* Advance all replicas by n_steps >= 0 (asynchronous on the context stream). */
@@ -287,6 +291,11 @@ cph_status cph_get_dbo_stats(cph_ctx *ctx, int32_t replica, double *well, double
  *   E_p = pH-dependent bias (VpH + Vdw at level p's PFC depths), kJ/mol, fp64.
  * cph_exchange_apply: rows_all [remd_total*(P+1)]; pairs (p, p+1), p = attempt mod 2,
  *   +2, ...; accept with min(1, exp(-Delta/kT)), u from Philox(seed; attempt, ladder, p, 5). */
+/* Labels that do not form ladders (a level missing or held twice in a ladder, or out of
+ * range) make cph_exchange_apply a no-op and latch CPH_E_STATE (reported by the next sync).
+ * Ordering: both calls are enqueued on the context stream (cph_get_stream); a caller that
+ * fills or reads the row buffers on another stream (e.g. NCCL on torch's current stream)
+ * must order the two streams with events around the calls (the Python binding does). */
 cph_status cph_exchange_energies(cph_ctx *ctx, double *rows);
 cph_status cph_exchange_apply(cph_ctx *ctx, const double *rows_all, uint64_t seed, int64_t attempt);
 /* Single-context shortcut (remd_total == R): energies + apply on an internal buffer. */
@@ -308,12 +317,35 @@ cph_status cph_get_positions(cph_ctx *ctx, int32_t replica, float *pos, float *v
  * indices) with float32 d^2 < rlist^2, lexicographically sorted, as [2*n].
  * If cap < n nothing is written and *n tells the size needed. */
 cph_status cph_get_pairlist(cph_ctx *ctx, int32_t replica, int32_t *pairs, int64_t cap, int64_t *n);
+/* Every directed entry (i, j) (original indices) the pair kernel evaluates from the last
+ * rebuild's list, sorted lexicographically, as [2*n]; each canonical pair (i, j) of
+ * cph_get_pairlist must appear exactly twice, as (i, j) and (j, i) (the kernel's list is
+ * full, both directions; SURVEY §8(c) "pair lists bit-exact").  Same size protocol. */
+cph_status cph_get_pairlist_directed(cph_ctx *ctx, int32_t replica, int32_t *pairs, int64_t cap, int64_t *n);
+/* Rows of that directed list for selected atoms (for large systems): for atoms[k]
+ * (original index) its partners j, sorted ascending, are cols[row_ptr[k] .. row_ptr[k+1]).
+ * row_ptr [n_atoms+1] is always filled; cols [cap] only up to cap entries (call again with
+ * cap >= row_ptr[n_atoms] to get all).  CPH_E_INVALID on an out-of-range atom. */
+cph_status cph_get_pairlist_rows(cph_ctx *ctx, int32_t replica, const int32_t *atoms, int32_t n_atoms,
+                                 int32_t *row_ptr, int32_t *cols, int64_t cap);
+/* The device's lambda-group CSR mapped back to original atom indices (north star: lambda-group
+ * indexing bit-exact): group_ptr / coord_ptr [G+1] as stored on the device; atoms[k] = the
+ * original index reached from lambda slot k through the device's sorted-slot permutation
+ * (iperm then meta); slot_atoms[k] = the original index of the sorted slot whose meta word
+ * carries lambda slot k (-1 if none).  Both must equal the input group_atoms. */
+cph_status cph_get_lambda_groups(cph_ctx *ctx, int32_t replica, int32_t *group_ptr, int32_t *coord_ptr,
+                                 int32_t *atoms /*[n_lambda]*/, int32_t *slot_atoms /*[n_lambda]*/);
 /* Fixed-lambda TI (mode 1): mean of the Coulomb dV/dlambda = f sum (dq/dl) phi per
  * coordinate over the steps completed since create or the last cph_set_state(_all)
  * (which restart the accumulators), and the number of samples; this is the
  * <dH_ref/dlambda> = <dV_coul/dlambda> the Vmm calibration fits. */
 cph_status cph_get_ti_means(cph_ctx *ctx, int32_t replica, double *mean /*[C]*/, int64_t *n_samples);
-/* Checkpoint of one replica: size query with buf == NULL (*n gets bytes). */
+/* Checkpoint of one replica: size query with buf == NULL (*n gets bytes).  The blob carries
+ * the step (Philox counters, frame / nstlist / DBO phases count from it).  cph_set_state
+ * (one replica) requires the blob's step to equal the context's current step
+ * (CPH_E_STATE otherwise); cph_set_state_all (every replica) requires all blobs to carry
+ * the same step and moves the context's clock to it, so a restore into a fresh context
+ * continues the run. */
 cph_status cph_get_state(cph_ctx *ctx, int32_t replica, void *buf, int64_t cap, int64_t *n);
 cph_status cph_set_state(cph_ctx *ctx, int32_t replica, const void *buf, int64_t n);
 

@@ -152,7 +152,8 @@ class OracleReplica:
     def evaluate(self, x, lam):
         s, p = self.sys, self.p
         q, dq = charges(s, lam)
-        rs = real_space(x, q, s.type, s.c6, s.c12, self.box, p["rc"], self.beta, s.excl)
+        rs = real_space(x, q, s.type, s.c6, s.c12, self.box, p["rc"], self.beta, s.excl,
+                        max_chunks=p.get("sample_real_chunks"))    # bench.py CPU sample only
         ex = exclusion_correction(x, q, self.box, self.beta, s.excl)
         e_self, phi_self = self_term(q, self.beta)
         e_net, phi_net = net_charge_term(q, self.box, self.beta)

@@ -44,11 +44,14 @@ def _excl_keys(excl, n):
     return np.unique(i * n + j)
 
 
-def real_space(pos, q, types, c6, c12, box, rc, beta, excl, want_lj=True, chunk=256):
+def real_space(pos, q, types, c6, c12, box, rc, beta, excl, want_lj=True, chunk=256, max_chunks=None):
     """Brute-force all-pairs real-space Ewald + LJ within rc (min image).
 
     Returns dict(E_LJ, E_real, phi (N,), F (N,3)) where phi is the real-space
-    potential (e/nm, without f) and F the real-space Coulomb + LJ force."""
+    potential (e/nm, without f) and F the real-space Coulomb + LJ force.
+    max_chunks (bench.py's bounded CPU sample only): stop after that many row chunks of
+    `chunk` atoms i (each chunk costs the same: all j are tested); the result is then
+    partial and only its run time is used."""
     pos = np.asarray(pos, np.float64)
     n = len(pos)
     keys = _excl_keys(np.asarray(excl).reshape(-1, 2), n)
@@ -58,7 +61,9 @@ def real_space(pos, q, types, c6, c12, box, rc, beta, excl, want_lj=True, chunk=
     e_re = 0.0
     rc2 = rc * rc
     two_b_sqpi = 2.0 * beta / math.sqrt(math.pi)
-    for i0 in range(0, n, chunk):
+    for c_idx, i0 in enumerate(range(0, n, chunk)):
+        if max_chunks is not None and c_idx >= max_chunks:
+            break
         i1 = min(n, i0 + chunk)
         ii = np.arange(i0, i1)
         d = pos[None, :, :] - pos[ii, None, :]              # r_j - r_i

@@ -41,3 +41,31 @@ def canonical_pairs(pos, box, rlist, excl=None, chunk=512):
         pairs = pairs[~np.isin(pk, ek)]
     order = np.lexsort((pairs[:, 1], pairs[:, 0]))
     return pairs[order]
+
+
+def canonical_partners(pos, box, rlist, excl, idx):
+    """Rows of the canonical list for selected atoms: for each i in idx the sorted array of
+    j != i (non-excluded) with {min(i,j), max(i,j)} in canonical_pairs.  Same fp32 formula;
+    evaluated as dx = x_j - x_i for every j, which equals the canonical orientation up to an
+    exact sign flip (IEEE subtraction, rint half-to-even and L * k are odd functions), so
+    d2 is bit-identical.  Used for sampled rows at sizes the all-pairs list cannot reach."""
+    p = np.asarray(pos, dtype=np.float32)
+    n = len(p)
+    L = np.asarray(box, dtype=np.float64).astype(np.float32)
+    invL = np.float32(1.0) / L
+    rl2 = np.float32(rlist) * np.float32(rlist)
+    e = np.asarray(excl if excl is not None else np.zeros((0, 2)), np.int64).reshape(-1, 2)
+    rows = []
+    for i in idx:
+        d2 = None
+        for dim in range(3):
+            dx = p[:, dim] - p[i, dim]
+            dx = dx - L[dim] * np.rint(dx * invL[dim])
+            sq = dx * dx
+            d2 = sq if d2 is None else (d2 + sq)
+        m = d2 < rl2
+        m[i] = False
+        ex = np.concatenate([e[e[:, 0] == i, 1], e[e[:, 1] == i, 0]])
+        m[ex] = False
+        rows.append(np.nonzero(m)[0].astype(np.int64))
+    return rows

@@ -73,6 +73,7 @@ EXPORTS = {
     "cph_default_params": (None, [_p(cph_params)]),
     "cph_create": (C.c_int, [_p(cph_system), _p(cph_params), _p(C.c_void_p)]),
     "cph_destroy": (None, [C.c_void_p]),
+    "cph_get_stream": (C.c_void_p, [C.c_void_p]),
     "cph_n_coords": (C.c_int32, [C.c_void_p]),
     "cph_n_atoms": (C.c_int32, [C.c_void_p]),
     "cph_n_replicas": (C.c_int32, [C.c_void_p]),
@@ -100,6 +101,9 @@ EXPORTS = {
     "cph_get_forces": (C.c_int, [C.c_void_p, C.c_int32, _f32p, _f32p]),
     "cph_get_positions": (C.c_int, [C.c_void_p, C.c_int32, _f32p, _f32p]),
     "cph_get_pairlist": (C.c_int, [C.c_void_p, C.c_int32, _i32p, C.c_int64, _i64p]),
+    "cph_get_pairlist_directed": (C.c_int, [C.c_void_p, C.c_int32, _i32p, C.c_int64, _i64p]),
+    "cph_get_lambda_groups": (C.c_int, [C.c_void_p, C.c_int32, _i32p, _i32p, _i32p, _i32p]),
+    "cph_get_pairlist_rows": (C.c_int, [C.c_void_p, C.c_int32, _i32p, C.c_int32, _i32p, _i32p, C.c_int64]),
     "cph_get_ti_means": (C.c_int, [C.c_void_p, C.c_int32, _f64p, _i64p]),
     "cph_get_state": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, _i64p]),
     "cph_set_state": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]),
@@ -163,6 +167,15 @@ def _torch_allocator(device):
     return ALLOC_FN(alloc), FREE_FN(free)
 
 
+_FLOAT_PARAMS = ("dt", "temperature", "gamma_atom", "gamma_lambda", "lambda_mass", "rc", "rlist", "ewald_rtol",
+                 "barrier", "wall_k", "tau_atom", "tau_lambda", "dbo_well_near", "dbo_residency", "dbo_well_tol",
+                 "dbo_well_gain", "dbo_well_cap", "dbo_trans_lo", "dbo_trans_hi", "dbo_target", "dbo_target_tol",
+                 "dbo_barrier_step", "dbo_barrier_min", "dbo_barrier_max")
+_INT_PARAMS = ("pme_order", "nstlist", "nstout", "nstenergy", "frame_capacity", "dbo_well", "dbo_barrier",
+               "dbo_well_steps", "dbo_barrier_steps", "dbo_censor_steps", "hamiltonian")
+KNOWN_PARAMS = frozenset(_FLOAT_PARAMS + _INT_PARAMS + ("thermostat", "pme_grid"))
+
+
 def cph_create(system, pH, replica_seed, *, lambda0=None, pos_replicas=None, vel_replicas=None, device=0,
                mode=0, cuda_stream=None, use_torch_allocator=True, ph_levels=None, remd_first=0, remd_total=0,
                **overrides):
@@ -214,24 +227,20 @@ def cph_create(system, pH, replica_seed, *, lambda0=None, pos_replicas=None, vel
     p.n_replicas = R
     p.device = device
     p.mode = mode
+    unknown = sorted(set(overrides) - KNOWN_PARAMS)
+    if unknown:                     # SPEC.md:77 "unknown keys are errors"
+        raise ValueError(f"unknown cph_params override(s): {', '.join(unknown)}")
     params = dict(getattr(system, "params", {}))
     params.update(overrides)
-    for k in ("dt", "temperature", "gamma_atom", "gamma_lambda", "lambda_mass", "rc", "rlist", "ewald_rtol",
-              "barrier", "wall_k"):
+    for k in _FLOAT_PARAMS:
         if k in params:
             setattr(p, k, float(params[k]))
-    for k in ("pme_order", "nstlist", "nstout", "nstenergy", "frame_capacity", "dbo_well", "dbo_barrier",
-              "dbo_well_steps", "dbo_barrier_steps", "dbo_censor_steps", "hamiltonian"):
+    for k in _INT_PARAMS:
         if k in params:
             setattr(p, k, int(params[k]))
     if "thermostat" in params:
         t = params["thermostat"]
         p.thermostat = {"langevin": 0, "bussi": 1}[t] if isinstance(t, str) else int(t)
-    for k in ("tau_atom", "tau_lambda", "dbo_well_near", "dbo_residency", "dbo_well_tol", "dbo_well_gain",
-              "dbo_well_cap", "dbo_trans_lo", "dbo_trans_hi", "dbo_target", "dbo_target_tol", "dbo_barrier_step",
-              "dbo_barrier_min", "dbo_barrier_max"):
-        if k in params:
-            setattr(p, k, float(params[k]))
     grid = overrides.get("pme_grid", getattr(system, "pme_grid", None))
     if grid is not None:
         p.pme_grid[:] = [int(g) for g in grid]
@@ -360,16 +369,32 @@ class Context:
         import torch
         return torch.device("cuda", self.device)
 
+    def lib_stream(self):
+        """The context's CUDA stream as a torch stream object (cph_get_stream)."""
+        import torch
+        return torch.cuda.ExternalStream(int(lib().cph_get_stream(self.h) or 0), device=self.exchange_device())
+
     def exchange_energies_into(self, t):
-        """Write this context's (label, E_p) rows into the float64 CUDA tensor t."""
+        """Write this context's (label, E_p) rows into the float64 CUDA tensor t.  Ordered
+        after torch's current stream (which allocated / last used t) and before it (which
+        runs the NCCL gather): the library writes on its own stream."""
         import torch
         assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and t.numel() >= self.R * (self.P + 1)
+        cur, ls = torch.cuda.current_stream(t.device), self.lib_stream()
+        ls.wait_stream(cur)
+        t.record_stream(ls)
         self.cph_exchange_energies(t.data_ptr())
+        cur.wait_stream(ls)
 
     def exchange_apply_from(self, t, seed, attempt):
+        """Apply the decisions from the gathered rows t (filled on torch's current stream)."""
         import torch
         assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+        cur, ls = torch.cuda.current_stream(t.device), self.lib_stream()
+        ls.wait_stream(cur)
+        t.record_stream(ls)
         self.cph_exchange_apply(t.data_ptr(), seed, attempt)
+        cur.wait_stream(ls)
 
     def cph_get_labels(self):
         lab = np.zeros(self.R, np.int32)
@@ -432,6 +457,34 @@ class Context:
         out = np.zeros(2 * max(n.value, 1), np.int32)
         _check(lib().cph_get_pairlist(self.h, r, _ptr(out, C.c_int32), n.value, C.byref(n)), self.h)
         return out[: 2 * n.value].reshape(-1, 2)
+
+    def cph_get_pairlist_directed(self, r):
+        n = C.c_int64()
+        _check(lib().cph_get_pairlist_directed(self.h, r, None, 0, C.byref(n)), self.h)
+        out = np.zeros(2 * max(n.value, 1), np.int32)
+        _check(lib().cph_get_pairlist_directed(self.h, r, _ptr(out, C.c_int32), n.value, C.byref(n)), self.h)
+        return out[: 2 * n.value].reshape(-1, 2)
+
+    def cph_get_pairlist_rows(self, r, atoms):
+        """List of sorted partner arrays (original indices) for each original atom index."""
+        a = np.ascontiguousarray(atoms, np.int32)
+        ptr = np.zeros(len(a) + 1, np.int32)
+        _check(lib().cph_get_pairlist_rows(self.h, r, _ptr(a, C.c_int32), len(a), _ptr(ptr, C.c_int32), None, 0),
+               self.h)
+        cols = np.zeros(max(int(ptr[-1]), 1), np.int32)
+        _check(lib().cph_get_pairlist_rows(self.h, r, _ptr(a, C.c_int32), len(a), _ptr(ptr, C.c_int32),
+                                           _ptr(cols, C.c_int32), int(ptr[-1])), self.h)
+        return [cols[ptr[k]:ptr[k + 1]].copy() for k in range(len(a))]
+
+    def cph_get_lambda_groups(self, r, n_groups, n_lambda):
+        """(group_ptr, coord_ptr, atoms via iperm, atoms via meta) as stored on the device."""
+        gp = np.zeros(n_groups + 1, np.int32)
+        cp = np.zeros(n_groups + 1, np.int32)
+        a = np.zeros(max(n_lambda, 1), np.int32)
+        b = np.zeros(max(n_lambda, 1), np.int32)
+        _check(lib().cph_get_lambda_groups(self.h, r, _ptr(gp, C.c_int32), _ptr(cp, C.c_int32), _ptr(a, C.c_int32),
+                                           _ptr(b, C.c_int32)), self.h)
+        return gp, cp, a[:n_lambda], b[:n_lambda]
 
     def cph_get_ti_means(self, r):
         m = np.zeros(self.C)

@@ -30,7 +30,7 @@ constexpr int kMaxAtoms = 1 << 21;
 
 // Device-side flags (int array)
 enum { FLAG_PENDING_CLOSE = 0, FLAG_LIST_OVERFLOW = 1, FLAG_DIVERGED = 2, FLAG_MAX_NNB = 3,
-       FLAG_STEP_DONE = 4, FLAG_BAD_STATE = 5, FLAG_COUNT = 8 };
+       FLAG_STEP_DONE = 4, FLAG_BAD_STATE = 5, FLAG_REMD_BAD = 6, FLAG_COUNT = 8 };
 
 // Scalars every kernel needs, passed by value.
 struct KParams {

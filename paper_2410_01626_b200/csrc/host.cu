@@ -12,9 +12,19 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "cph_device.cuh"
 
 using namespace cph;
+
+// NVTX ranges (header-only nvtx3): one per API call and per kernel class of an eagerly
+// enqueued step, so an nsys / ncu --nvtx timeline attributes every launch
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define CPH_NVTX(name) NvtxRange nvtx_range_(name)
 
 struct cph_ctx {
   Ctx c;
@@ -245,6 +255,7 @@ static void tl_print(Ctx &c) {
 
 // one full step (n -> n+1) on the context streams; returns kernels launched
 int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
+  CPH_NVTX(rebuild ? "cph step (rebuild)" : "cph step");
   int k = 0;
   cudaStream_t s = c.stream;
   tl_mark(c, s, 0);
@@ -306,6 +317,7 @@ int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
 
 // evaluation at the current state without integration (create / set_state)
 cph_status evaluate_here(Ctx &c) {
+  CPH_NVTX("evaluate_here");
   cudaStream_t s = c.stream;
   k_set_end<<<1, 1, 0, s>>>(c.d.end_step, c.host_step);
   CK(cudaMemsetAsync(c.d.erec + (size_t)(c.host_step & 1) * c.kp.R * kNE, 0, sizeof(double) * c.kp.R * kNE, s));
@@ -338,6 +350,10 @@ cph_status check_flags(Ctx &c) {
     c.err = "lambda diverged (|lambda| > 10 or non-finite dV/dlambda)";
     return CPH_E_DIVERGED;
   }
+  if (f[FLAG_REMD_BAD]) {
+    c.err = "replica exchange: gathered labels do not form ladders (a level missing or held twice); no swap was made";
+    return CPH_E_STATE;
+  }
   if (f[FLAG_LIST_OVERFLOW]) {
     char buf[160];
     snprintf(buf, sizeof buf, "pair list overflow: %d neighbours > capacity %d; results since the last rebuild are invalid",
@@ -369,6 +385,21 @@ cph_status capture_block(Ctx &c) {
   cudaGraphDestroy(g);
   c.graph_block_kernels = k;
   return CPH_OK;
+}
+
+// Every ladder (P consecutive global replicas) that lies entirely inside [first, first + R)
+// must hold each level 0..P-1 exactly once (R29); partially held ladders are checked
+// on the device at each exchange (k_remd_apply).
+bool labels_form_ladders(const int *labels, int R, int first, int P) {
+  for (int l0 = (first + P - 1) / P * P; l0 + P <= first + R; l0 += P) {
+    std::vector<char> seen(P, 0);
+    for (int g = l0; g < l0 + P; ++g) {
+      const int lab = labels[g - first];
+      if (lab < 0 || lab >= P || seen[lab]) return false;
+      seen[lab] = 1;
+    }
+  }
+  return true;
 }
 
 cph_status check_replica(Ctx &c, int r) {
@@ -440,6 +471,7 @@ static cph_status fail_create(cph_ctx *ctx, cph_status st) {
 }
 
 cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **out) {
+  CPH_NVTX("cph_create");
   if (!out) { g_create_err = "out is NULL"; return CPH_E_INVALID; }
   *out = nullptr;
   if (!sys || !prm) { g_create_err = "system/params is NULL"; return CPH_E_INVALID; }
@@ -498,6 +530,8 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
       labels0.push_back(lab);
     }
     c.h_levels.assign(prm->ph_levels, prm->ph_levels + P);
+    if (!labels_form_ladders(labels0.data(), R, prm->remd_first, P))
+      return bad("each pH ladder held by this context must carry every level exactly once");
   }
   if (prm->dbo_well || prm->dbo_barrier) {
     if ((prm->dbo_well && (prm->dbo_well_steps < 1 || prm->dbo_well_steps % prm->nstlist)) ||
@@ -964,6 +998,7 @@ void cph_destroy(cph_ctx *ctx) {
   delete ctx;
 }
 
+void *cph_get_stream(const cph_ctx *ctx) { return ctx ? (void *)ctx->c.stream : nullptr; }
 int32_t cph_n_coords(const cph_ctx *ctx) { return ctx ? ctx->c.kp.C : -1; }
 int32_t cph_n_atoms(const cph_ctx *ctx) { return ctx ? ctx->c.kp.N : -1; }
 int32_t cph_n_replicas(const cph_ctx *ctx) { return ctx ? ctx->c.kp.R : -1; }
@@ -971,6 +1006,7 @@ int64_t cph_current_step(const cph_ctx *ctx) { return ctx ? ctx->c.host_step : -
 int64_t cph_launch_count(const cph_ctx *ctx) { return ctx ? ctx->c.launches : -1; }
 
 cph_status cph_set_pH(cph_ctx *ctx, int32_t replica, double pH) {
+  CPH_NVTX("cph_set_pH");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, replica);
@@ -982,8 +1018,15 @@ cph_status cph_set_pH(cph_ctx *ctx, int32_t replica, double pH) {
   const double old = c.h_pH[replica];
   c.h_pH[replica] = pH;
   st = run_pfc(c, replica);
-  if (st != CPH_OK) c.h_pH[replica] = old;
-  return st;
+  if (st != CPH_OK) {
+    c.h_pH[replica] = old;
+    return st;
+  }
+  // dV_bias/dlambda and E_bias at the unchanged lambda under the new pH tables, so the next
+  // half kick and the getters see the new Hamiltonian (the Coulomb part is unchanged)
+  c.launches += launch_bias_refresh(c, c.stream);
+  CK(cudaGetLastError());
+  return check_flags(c);
 }
 
 // steps host_step -> end as one asynchronous segment (graphs of nstlist steps where aligned)
@@ -1032,6 +1075,7 @@ static double barrier_decide(const DboConfig &b, double h, double n, double n_tr
 // adjusted sites, refresh their PFC and re-evaluate the forces at the unchanged state so
 // step S+1 starts on the new bias.
 static cph_status dbo_block_end(Ctx &c) {
+  CPH_NVTX("dbo_block_end");
   const KParams &kp = c.kp;
   const DboConfig &b = c.dbo;
   const long long S = c.host_step;
@@ -1107,6 +1151,7 @@ static long long next_dbo_boundary(const Ctx &c) {
 }
 
 cph_status cph_step(cph_ctx *ctx, int64_t n_steps) {
+  CPH_NVTX("cph_step");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   if (n_steps < 0) { c.err = "n_steps < 0"; return CPH_E_INVALID; }
@@ -1123,12 +1168,14 @@ cph_status cph_step(cph_ctx *ctx, int64_t n_steps) {
 }
 
 cph_status cph_sync(cph_ctx *ctx) {
+  CPH_NVTX("cph_sync");
   if (!ctx) return CPH_E_INVALID;
   cudaSetDevice(ctx->c.device);
   return check_flags(ctx->c);
 }
 
 cph_status cph_get_lambdas(cph_ctx *ctx, int32_t r, double *lam, double *vel) {
+  CPH_NVTX("cph_get_lambdas");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
@@ -1140,6 +1187,7 @@ cph_status cph_get_lambdas(cph_ctx *ctx, int32_t r, double *lam, double *vel) {
 }
 
 cph_status cph_get_dvdl(cph_ctx *ctx, int32_t r, double *coul, double *bias) {
+  CPH_NVTX("cph_get_dvdl");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
@@ -1165,6 +1213,7 @@ cph_status cph_get_bias_params(cph_ctx *ctx, int32_t r, double *d1) {
 }
 
 cph_status cph_get_energies(cph_ctx *ctx, int32_t r, double *e) {
+  CPH_NVTX("cph_get_energies");
   if (!ctx || !e) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
@@ -1179,6 +1228,7 @@ cph_status cph_get_energies(cph_ctx *ctx, int32_t r, double *e) {
 
 cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t r, float *buf, uint8_t *censored, int64_t *steps, int32_t *labels,
                              int64_t cap, int64_t *n_frames, int64_t *n_dropped) {
+  CPH_NVTX("cph_get_frames_ex");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
@@ -1227,6 +1277,7 @@ static cph_status need_remd(Ctx &c) {
 }
 
 cph_status cph_exchange_energies(cph_ctx *ctx, double *rows) {
+  CPH_NVTX("cph_exchange_energies");
   if (!ctx || !rows) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   if (cph_status st = need_remd(c)) return st;
@@ -1237,6 +1288,7 @@ cph_status cph_exchange_energies(cph_ctx *ctx, double *rows) {
 }
 
 cph_status cph_exchange_apply(cph_ctx *ctx, const double *rows_all, uint64_t seed, int64_t attempt) {
+  CPH_NVTX("cph_exchange_apply");
   if (!ctx || !rows_all || attempt < 0) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   if (cph_status st = need_remd(c)) return st;
@@ -1266,12 +1318,17 @@ cph_status cph_get_labels(cph_ctx *ctx, int32_t *labels) {
 }
 
 cph_status cph_set_labels(cph_ctx *ctx, const int32_t *labels) {
+  CPH_NVTX("cph_set_labels");
   if (!ctx || !labels) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = need_remd(c);
   if (st) return st;
   for (int r = 0; r < c.kp.R; ++r)
     if (labels[r] < 0 || labels[r] >= c.kp.P) { c.err = "label out of range"; return CPH_E_INVALID; }
+  if (!labels_form_ladders(labels, c.kp.R, c.kp.remd_first, c.kp.P)) {
+    c.err = "each pH ladder held by this context must carry every level exactly once";
+    return CPH_E_INVALID;
+  }
   cudaSetDevice(c.device);
   CK(cudaStreamSynchronize(c.stream));
   std::vector<int> lab(labels, labels + c.kp.R);
@@ -1301,6 +1358,7 @@ cph_status cph_get_dbo_params(cph_ctx *ctx, int32_t r, double *p) {
 }
 
 cph_status cph_set_dbo_params(cph_ctx *ctx, int32_t r, const double *p) {
+  CPH_NVTX("cph_set_dbo_params");
   if (!ctx || !p) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
@@ -1346,6 +1404,7 @@ cph_status cph_get_dbo_stats(cph_ctx *ctx, int32_t r, double *well, double *barr
 }
 
 cph_status cph_get_forces(cph_ctx *ctx, int32_t r, float *f, float *phi) {
+  CPH_NVTX("cph_get_forces");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
@@ -1385,6 +1444,7 @@ cph_status cph_get_forces(cph_ctx *ctx, int32_t r, float *f, float *phi) {
 }
 
 cph_status cph_get_positions(cph_ctx *ctx, int32_t r, float *pos, float *vel) {
+  CPH_NVTX("cph_get_positions");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
@@ -1403,32 +1463,144 @@ cph_status cph_get_positions(cph_ctx *ctx, int32_t r, float *pos, float *vel) {
   return CPH_OK;
 }
 
+}  // extern "C"
+
+// Pair-list decoding for the getters (host side).  The device list of replica r is copied
+// once; row(slot) gives the original indices of every entry the pair kernel evaluates for
+// that sorted slot (padding entries, which point at the atom itself, are skipped).
+struct ListHost {
+  std::vector<int> nnb;
+  std::vector<int2> meta;
+  std::vector<int> iperm;
+  std::vector<uint32_t> nbl;
+};
+
+static cph_status fetch_list(Ctx &c, int r, ListHost &h) {
+  const KParams &kp = c.kp;
+  const size_t N = kp.N, base = (size_t)r * kp.Nst;
+  h.nnb.resize(N);
+  h.meta.resize(N);
+  h.iperm.resize(N);
+  h.nbl.resize((size_t)kp.cap * kp.Nst);
+  CK(cudaMemcpy(h.nnb.data(), c.d.nnb + base, sizeof(int) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(h.meta.data(), c.d.meta + base, sizeof(int2) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(h.iperm.data(), c.d.iperm + (size_t)r * N, sizeof(int) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(h.nbl.data(), c.d.nbl + (size_t)r * kp.cap * kp.Nst, sizeof(uint32_t) * h.nbl.size(),
+                cudaMemcpyDeviceToHost));
+  return CPH_OK;
+}
+
+template <class F>
+static void list_row(const Ctx &c, const ListHost &h, int slot, F emit) {
+  const KParams &kp = c.kp;
+  for (int k = 0; k < std::min(h.nnb[slot], kp.cap); ++k) {
+    const int j = (int)(h.nbl[((size_t)(k / 8) * kp.Nst + slot) * 8 + (k % 8)] & kEntryJMask);
+    if (j != slot) emit(h.meta[j].x);
+  }
+}
+
+static cph_status decode_directed(Ctx &c, int r, std::vector<std::pair<int, int>> &out) {
+  ListHost h;
+  if (cph_status st = fetch_list(c, r, h)) return st;
+  out.clear();
+  for (int i = 0; i < c.kp.N; ++i) {
+    const int oi = h.meta[i].x;
+    list_row(c, h, i, [&](int oj) { out.emplace_back(oi, oj); });
+  }
+  return CPH_OK;
+}
+
+extern "C" {
+
+cph_status cph_get_pairlist_rows(cph_ctx *ctx, int32_t r, const int32_t *atoms, int32_t n_atoms, int32_t *row_ptr,
+                                 int32_t *cols, int64_t cap) {
+  CPH_NVTX("cph_get_pairlist_rows");
+  if (!ctx || !atoms || !row_ptr || n_atoms < 0 || cap < 0) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  for (int k = 0; k < n_atoms; ++k)
+    if (atoms[k] < 0 || atoms[k] >= c.kp.N) { c.err = "atom index out of range"; return CPH_E_INVALID; }
+  ListHost h;
+  if ((st = fetch_list(c, r, h))) return st;
+  int64_t n = 0;
+  row_ptr[0] = 0;
+  std::vector<int> row;
+  for (int k = 0; k < n_atoms; ++k) {
+    row.clear();
+    list_row(c, h, h.iperm[atoms[k]], [&](int oj) { row.push_back(oj); });
+    std::sort(row.begin(), row.end());
+    for (int oj : row) {
+      if (cols && n < cap) cols[n] = oj;
+      ++n;
+    }
+    if (n > INT32_MAX) { c.err = "row total exceeds int32"; return CPH_E_INVALID; }
+    row_ptr[k + 1] = (int32_t)n;
+  }
+  return CPH_OK;
+}
+
+static cph_status emit_pairs(std::vector<std::pair<int, int>> &out, int32_t *pairs, int64_t cap, int64_t *n) {
+  std::sort(out.begin(), out.end());
+  *n = (int64_t)out.size();
+  if (pairs && cap >= (int64_t)out.size())
+    for (size_t k = 0; k < out.size(); ++k) { pairs[2 * k] = out[k].first; pairs[2 * k + 1] = out[k].second; }
+  return CPH_OK;
+}
+
 cph_status cph_get_pairlist(cph_ctx *ctx, int32_t r, int32_t *pairs, int64_t cap, int64_t *n) {
+  CPH_NVTX("cph_get_pairlist");
   if (!ctx || !n) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  std::vector<std::pair<int, int>> all;
+  if ((st = decode_directed(c, r, all))) return st;
+  std::vector<std::pair<int, int>> out;
+  for (auto &p : all)
+    if (p.first < p.second) out.push_back(p);
+  return emit_pairs(out, pairs, cap, n);
+}
+
+cph_status cph_get_pairlist_directed(cph_ctx *ctx, int32_t r, int32_t *pairs, int64_t cap, int64_t *n) {
+  CPH_NVTX("cph_get_pairlist_directed");
+  if (!ctx || !n) return CPH_E_INVALID;
+  Ctx &c = ctx->c;
+  cph_status st = check_replica(c, r);
+  if (st || (st = cph_sync(ctx))) return st;
+  std::vector<std::pair<int, int>> all;
+  if ((st = decode_directed(c, r, all))) return st;
+  return emit_pairs(all, pairs, cap, n);
+}
+
+cph_status cph_get_lambda_groups(cph_ctx *ctx, int32_t r, int32_t *group_ptr, int32_t *coord_ptr, int32_t *atoms,
+                                 int32_t *slot_atoms) {
+  if (!ctx || !group_ptr || !coord_ptr || !atoms || !slot_atoms) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
   if (st || (st = cph_sync(ctx))) return st;
   const KParams &kp = c.kp;
   const size_t N = kp.N, base = (size_t)r * kp.Nst;
-  std::vector<int> nnb(N);
+  std::vector<int> iperm(N);
   std::vector<int2> meta(N);
-  std::vector<uint32_t> nbl((size_t)kp.cap * kp.Nst);
-  CK(cudaMemcpy(nnb.data(), c.d.nnb + base, sizeof(int) * N, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(iperm.data(), c.d.iperm + (size_t)r * N, sizeof(int) * N, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(meta.data(), c.d.meta + base, sizeof(int2) * N, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(nbl.data(), c.d.nbl + (size_t)r * kp.cap * kp.Nst, sizeof(uint32_t) * nbl.size(), cudaMemcpyDeviceToHost));
-  std::vector<std::pair<int, int>> out;
-  for (size_t i = 0; i < N; ++i) {
-    const int oi = meta[i].x;
-    for (int k = 0; k < std::min(nnb[i], kp.cap); ++k) {
-      const int j = (int)(nbl[((size_t)(k / 8) * kp.Nst + i) * 8 + (k % 8)] & kEntryJMask);
-      const int oj = meta[j].x;
-      if (oi < oj) out.emplace_back(oi, oj);
-    }
+  if (kp.G) {
+    CK(cudaMemcpy(group_ptr, c.d.g_ptr, sizeof(int) * (kp.G + 1), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(coord_ptr, c.d.g_cptr, sizeof(int) * (kp.G + 1), cudaMemcpyDeviceToHost));
+  } else {
+    group_ptr[0] = coord_ptr[0] = 0;
   }
-  std::sort(out.begin(), out.end());
-  *n = (int64_t)out.size();
-  if (pairs && cap >= (int64_t)out.size())
-    for (size_t k = 0; k < out.size(); ++k) { pairs[2 * k] = out[k].first; pairs[2 * k + 1] = out[k].second; }
+  std::vector<int> g_atoms(kp.nlam);
+  if (kp.nlam) CK(cudaMemcpy(g_atoms.data(), c.d.g_atoms, sizeof(int) * kp.nlam, cudaMemcpyDeviceToHost));
+  // device path 1: lambda slot k -> sorted slot (iperm of the stored atom) -> original index
+  for (int k = 0; k < kp.nlam; ++k) atoms[k] = meta[iperm[g_atoms[k]]].x;
+  // device path 2: the lambda slot each sorted slot's meta word carries -> original index
+  for (int k = 0; k < kp.nlam; ++k) slot_atoms[k] = -1;
+  for (size_t sl = 0; sl < N; ++sl) {
+    const int ls = (meta[sl].y >> 8) - 1;
+    if (ls >= 0 && ls < kp.nlam) slot_atoms[ls] = meta[sl].x;
+  }
   return CPH_OK;
 }
 
@@ -1476,6 +1648,7 @@ static cph_status get_states(Ctx &c, int r0, int nr, void *buf) {
 static cph_status set_states(Ctx &c, int r0, int nr, const void *buf, int64_t nbytes) {
   const size_t one = state_bytes(c);
   if (nbytes < (int64_t)(one * nr)) { c.err = "state blob too small"; return CPH_E_INVALID; }
+  int64_t blob_step = -1;
   for (int k = 0; k < nr; ++k) {
     int64_t hdr[4];
     std::memcpy(hdr, (const char *)buf + one * k, sizeof hdr);
@@ -1483,6 +1656,20 @@ static cph_status set_states(Ctx &c, int r0, int nr, const void *buf, int64_t nb
       c.err = "state blob does not match this context";
       return CPH_E_INVALID;
     }
+    if (hdr[3] < 0 || (k > 0 && hdr[3] != blob_step)) {
+      c.err = "state blobs carry different (or negative) steps";
+      return CPH_E_INVALID;
+    }
+    blob_step = hdr[3];
+  }
+  // The step is part of the state: the Philox noise is keyed on (seed, step) and frames,
+  // nstlist/nstout phases and DBO blocks count from it, so a restore continues the run.  The
+  // context has one clock: a full restore moves it, a partial one must match it.
+  const bool all = r0 == 0 && nr == c.kp.R;
+  if (!all && blob_step != c.host_step) {
+    c.err = "state blob step differs from the context's step (restore every replica with cph_set_state_all "
+            "to move the clock)";
+    return CPH_E_STATE;
   }
   cph_status st = ensure_state_buf(c);
   if (st) return st;
@@ -1498,6 +1685,12 @@ static cph_status set_states(Ctx &c, int r0, int nr, const void *buf, int64_t nb
     return CPH_E_INVALID;
   }
   c.launches += launch_unpack_state(c, c.stream, c.d.state_buf, (long long)one, r0, nr);
+  if (all && blob_step != c.host_step) {
+    c.host_step = blob_step;
+    const long long st64 = blob_step;
+    CK(cudaMemcpyAsync(c.d.step, &st64, sizeof(long long), cudaMemcpyHostToDevice, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+  }
   // a new configuration: TI accumulators restart
   CK(cudaMemsetAsync(c.d.ti_sum, 0, sizeof(double) * (size_t)c.kp.R * c.kp.C, c.stream));
   CK(cudaMemsetAsync(c.d.ti_n, 0, sizeof(long long), c.stream));
@@ -1506,6 +1699,7 @@ static cph_status set_states(Ctx &c, int r0, int nr, const void *buf, int64_t nb
 }
 
 cph_status cph_get_state(cph_ctx *ctx, int32_t r, void *buf, int64_t cap, int64_t *n) {
+  CPH_NVTX("cph_get_state");
   if (!ctx || !n) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
@@ -1519,6 +1713,7 @@ cph_status cph_get_state(cph_ctx *ctx, int32_t r, void *buf, int64_t cap, int64_
 }
 
 cph_status cph_set_state(cph_ctx *ctx, int32_t r, const void *buf, int64_t nbytes) {
+  CPH_NVTX("cph_set_state");
   if (!ctx || !buf) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
@@ -1527,6 +1722,7 @@ cph_status cph_set_state(cph_ctx *ctx, int32_t r, const void *buf, int64_t nbyte
 }
 
 cph_status cph_get_state_all(cph_ctx *ctx, void *buf, int64_t cap, int64_t *n) {
+  CPH_NVTX("cph_get_state_all");
   if (!ctx || !n) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   *n = (int64_t)(state_bytes(c) * c.kp.R);
@@ -1539,6 +1735,7 @@ cph_status cph_get_state_all(cph_ctx *ctx, void *buf, int64_t cap, int64_t *n) {
 }
 
 cph_status cph_set_state_all(cph_ctx *ctx, const void *buf, int64_t nbytes) {
+  CPH_NVTX("cph_set_state_all");
   if (!ctx || !buf) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cudaSetDevice(c.device);
@@ -1548,13 +1745,17 @@ cph_status cph_set_state_all(cph_ctx *ctx, const void *buf, int64_t nbytes) {
 }
 
 cph_status cph_profile_steps(cph_ctx *ctx, int64_t n_steps, double *ms, int64_t *launches) {
+  CPH_NVTX("cph_profile_steps");
   if (!ctx || n_steps < 0) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cudaSetDevice(c.device);
   cudaStream_t s = c.stream;
   std::vector<cudaEvent_t> evs;
   std::vector<int> cls;
+  static const char *kClassNames[] = {"integrate", "pairlist", "nonbonded", "spread", "fft_r2c", "solve",
+                                      "fft_c2r", "gather", "lambda", "hi"};
   auto mark = [&](int k) {
+    if (k >= 0 && k < (int)(sizeof(kClassNames) / sizeof(kClassNames[0]))) nvtxMarkA(kClassNames[k]);
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, s);

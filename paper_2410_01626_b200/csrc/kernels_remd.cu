@@ -35,12 +35,26 @@ __global__ void __launch_bounds__(1024) k_remd_apply(KParams kp, DevBufs d, cons
                                                      long long attempt) {
   const int P = kp.P, Rt = kp.remd_total, L = Rt / P;
   const int npair = (P - 1 - (int)(attempt & 1) + 1) / 2;       // pairs p = attempt%2, +2, ... < P-1
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  for (int g = threadIdx.x; g < Rt; g += blockDim.x) d.remd_holder[g] = -1;
+  __syncthreads();
+  // each ladder must hold every level once: a duplicated label (CAS finds the slot taken) or
+  // a missing one (slot still -1 below) makes the attempt a no-op and raises FLAG_REMD_BAD
   for (int g = threadIdx.x; g < Rt; g += blockDim.x) {
-    const int lab = (int)rows[(size_t)g * (P + 1)];
-    d.remd_holder[(g / P) * P + lab] = g;
+    const double lv = rows[(size_t)g * (P + 1)];
+    const int lab = (int)lv;
+    if (!(lv >= 0.0 && lv < (double)P) || atomicCAS(&d.remd_holder[(g / P) * P + lab], -1, g) != -1) bad = 1;
     d.remd_newlab[g] = lab;
   }
   __syncthreads();
+  for (int g = threadIdx.x; g < Rt; g += blockDim.x)
+    if (d.remd_holder[g] < 0) bad = 1;
+  __syncthreads();
+  if (bad) {
+    if (threadIdx.x == 0) d.flags[FLAG_REMD_BAD] = 1;
+    return;
+  }
   const double beta = 1.0 / kp.kT;
   for (int t = threadIdx.x; t < L * npair; t += blockDim.x) {
     const int l = t / npair, p = (int)(attempt & 1) + 2 * (t % npair);

@@ -91,3 +91,22 @@ def test_invalid_dbo_params_rejected(cph):
         with pytest.raises(cph.CphError) as ei:
             cph.cph_create(s, [4.0], [1], use_torch_allocator=False, **kw)
         assert ei.value.status == 1 and "DBO" in str(ei.value), kw
+
+
+def test_unknown_override_rejected(cph):
+    """SPEC.md:77 "unknown keys are errors": a misspelt parameter never silently falls back
+    to its default."""
+    s = _sys()
+    with pytest.raises(ValueError, match="gama_atom"):
+        cph.cph_create(s, [4.0], [1], gama_atom=3.0, use_torch_allocator=False)
+
+
+@pytest.mark.parametrize("labels", [[0, 0, 1], [0, 2, 2], [1, 1, 1]])
+def test_replica_exchange_ladders_must_be_permutations(cph, labels):
+    """A ladder held by one context must carry every pH level exactly once (ADVICE r1:
+    duplicate labels would corrupt the level assignment in k_remd_apply)."""
+    s = _sys()
+    levels = [4.0, 5.0, 6.0]
+    with pytest.raises(cph.CphError) as ei:
+        cph.cph_create(s, [levels[k] for k in labels], [1, 2, 3], ph_levels=levels, use_torch_allocator=False)
+    assert ei.value.status == 1 and "ladder" in str(ei.value)

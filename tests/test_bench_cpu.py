@@ -9,7 +9,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_reference_arm_json_line():
-    env = dict(os.environ, CPH_REF_BUDGET_S="2")
+    env = dict(os.environ, CPH_REF_WORKERS="2")
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
                           "--warmup", "0", "--config", "1"], capture_output=True, text=True, env=env, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -23,3 +23,16 @@ def test_reference_arm_json_line():
     assert d["config"]["workload"].startswith("C1")
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_gpus_flag_never_runs_fewer_ranks():
+    """`bench.py --gpus 2` without torchrun starts 2 ranks itself, or fails (non-zero) when
+    fewer GPUs exist; it never silently runs one rank."""
+    import torch
+    if torch.cuda.device_count() >= 2:
+        return
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
+                          "--warmup", "3"], capture_output=True, text=True, timeout=600,
+                         env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert out.returncode != 0
+    assert "only" in out.stderr and not [ln for ln in out.stdout.splitlines() if ln.startswith("{")]

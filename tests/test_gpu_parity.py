@@ -41,20 +41,31 @@ def test_snapshot_parity(cph, which):
         print(which, r, {k: v for k, v in err.items() if k != "E_terms"})
         assert err["force"] <= RTOL
         assert err["phi"] <= RTOL
+        assert err["force_atom"] <= RTOL          # per atom: max_i |dF_i| / max(|F_i|, rms F)
+        assert err["phi_atom"] <= RTOL
         assert err["phi_lambda_atoms"] <= RTOL
         assert err["dvdl_coul"] <= RTOL
         assert err["dvdl_bias"] <= 1e-9
         assert err["E_total"] <= ETOL, err["E_terms"]
 
 
-@pytest.mark.parametrize("which", ["tiny", "c1", "c2"])
+def _check_directed(ctx, r, ref):
+    """The kernel's directed entries are exactly both orientations of the canonical set."""
+    dirs = ctx.cph_get_pairlist_directed(r)
+    both = np.concatenate([ref, ref[:, ::-1]])
+    both = both[np.lexsort((both[:, 1], both[:, 0]))]
+    assert dirs.shape == both.shape and np.array_equal(dirs, both)
+
+
+@pytest.mark.parametrize("which", ["tiny", "c1", "c2", "c3"])
 def test_pairlist_bit_exact(cph, which):
-    s = small_system() if which == "tiny" else make_system(1 if which == "c1" else 2)
+    s = small_system() if which == "tiny" else make_system({"c1": 1, "c2": 2, "c3": 3}[which])
     ctx, *_ = _ctx(cph, s, 2)
+    ref = OPL.canonical_pairs(s.pos, s.box, s.params["rlist"], s.excl)
     for r in range(2):
         got = ctx.cph_get_pairlist(r)
-        ref = OPL.canonical_pairs(s.pos, s.box, s.params["rlist"], s.excl)
         assert got.shape == ref.shape and np.array_equal(got, ref)
+    _check_directed(ctx, 1, ref)
     # after a rebuild at step nstlist, against the positions the device holds
     ctx.cph_step(s.params["nstlist"])
     for r in range(2):
@@ -62,6 +73,42 @@ def test_pairlist_bit_exact(cph, which):
         got = ctx.cph_get_pairlist(r)
         ref = OPL.canonical_pairs(x, s.box, s.params["rlist"], s.excl)
         assert np.array_equal(got, ref)
+        if r == 0:
+            _check_directed(ctx, r, ref)
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_pairlist_rows_full_size(cph, cfg):
+    """C4 (40k) and C5 (250k atoms, the bench's largest configs): sampled rows of the directed
+    list (2000 atoms incl. every lambda atom and solute exclusions) against the oracle's
+    canonical rows, at create and after a rebuild."""
+    s = make_system(cfg)
+    ctx = cph.cph_create(s, [5.0], [11], vel_replicas=make_velocities(s, 3)[None])
+    rng = np.random.default_rng(cfg)
+    idx = np.unique(np.concatenate([s.group_atoms, s.excl[:200, 0], rng.choice(s.n_atoms, 1800, replace=False)]))
+    for stage in range(2):
+        x = s.pos if stage == 0 else ctx.cph_get_positions(0)[0]
+        got = ctx.cph_get_pairlist_rows(0, idx)
+        ref = OPL.canonical_partners(x, s.box, s.params["rlist"], s.excl, idx)
+        bad = [int(i) for i, a, b in zip(idx, got, ref) if not np.array_equal(a, b)]
+        assert not bad, bad[:10]
+        ctx.cph_step(s.params["nstlist"])
+
+
+@pytest.mark.parametrize("which", ["c2", "c4"])
+def test_lambda_group_csr_bit_exact(cph, which):
+    """The device's lambda-group CSR, mapped back through its sorted-slot permutation to
+    original indices, equals the oracle's (north star: lambda-group indexing bit-exact), at
+    create and after rebuilds re-sorted the atoms."""
+    from oracle.charges import coord_ptr
+    s = make_system({"c2": 2, "c4": 4}[which])
+    ctx, *_ = _ctx(cph, s, 2)
+    for stage in range(2):
+        for r in range(2):
+            gp, cp, a, b = ctx.cph_get_lambda_groups(r, s.n_groups, len(s.group_atoms))
+            assert np.array_equal(gp, s.group_ptr) and np.array_equal(cp, coord_ptr(s.group_kind))
+            assert np.array_equal(a, s.group_atoms) and np.array_equal(b, s.group_atoms)
+        ctx.cph_step(3 * s.params["nstlist"])
 
 
 def test_pfc_matches_oracle(cph):
@@ -276,6 +323,9 @@ def test_full_size_sampled_parity(cph, cfg):
     F_ref = Fr + ex["F"][idx] + rec["F"][idx]
     assert np.linalg.norm(phi[idx] - phi_ref) / np.linalg.norm(phi_ref) < 2e-5
     assert np.linalg.norm(f[idx] - F_ref) / np.linalg.norm(F_ref) < 2e-5
+    from tests.parity import force_atom_err, phi_atom_err
+    print(f"C{cfg} per-atom F", force_atom_err(f[idx], F_ref), "phi", phi_atom_err(phi[idx], phi_ref))
+    assert force_atom_err(f[idx], F_ref) < 2e-5 and phi_atom_err(phi[idx], phi_ref) < 2e-5
     # dV/dlambda per coordinate from the sampled phi of every lambda atom
     pos = {a: k for k, a in enumerate(idx)}
     from oracle.charges import coord_ptr
@@ -353,3 +403,50 @@ def test_dense_region_grows_list_capacity_and_no_groups(cph):
     err = compare_snapshot(ctx, 0, oref)
     print({k: v for k, v in err.items() if k != "E_terms"})
     assert err["force"] <= RTOL and err["phi"] <= RTOL
+
+
+def test_set_ph_refreshes_bias_forces(cph):
+    """cph_set_pH re-evaluates dV_bias/dlambda and E_bias at the unchanged lambda:
+    right after the call both equal the oracle's at the new pH (fp64 on both sides)."""
+    s = make_system(2)
+    ctx, lam0, pH, seeds, vel = _ctx(cph, s, 2)
+    ctx.cph_step(7)
+    for r, new in ((0, 6.3), (1, 2.2)):
+        ctx.cph_set_pH(r, new)
+        lam, _ = ctx.cph_get_lambdas(r)
+        x, v = ctx.cph_get_positions(r)
+        ref = OracleReplica(s, new, int(seeds[r]), lam0=lam, vel0=v, pos0=x)
+        _, bias = ctx.cph_get_dvdl(r)
+        np.testing.assert_allclose(bias, ref.cur["dvdl_bias"], rtol=1e-9, atol=1e-9)
+        e = ctx.cph_get_energies(r)
+        assert abs(e["bias"] - ref.energies()["bias"]) < 1e-9 * max(1.0, abs(e["bias"]))
+
+
+def test_checkpoint_restore_continues_the_run(cph):
+    """A restore into a fresh context continues the run: the blob's step moves the
+    clock, so Philox noise, nstlist phases and frames pick up where they left off and the
+    trajectory matches the uninterrupted one (to the rounding of the fp32 spread atomics)."""
+    s = make_system(1)
+    R = 2
+    mk = lambda: _ctx(cph, s, R, seed=4)[0]
+    a = mk()
+    a.cph_step(25)
+    blob = a.cph_get_state_all()
+    a.cph_step(31)
+    b = mk()
+    b.cph_set_state_all(blob)
+    assert b.cph_current_step() == 25
+    b.cph_step(31)
+    assert b.cph_current_step() == a.cph_current_step() == 56
+    for r in range(R):
+        la, lb = a.cph_get_lambdas(r)[0], b.cph_get_lambdas(r)[0]
+        xa, xb = a.cph_get_positions(r)[0], b.cph_get_positions(r)[0]
+        d = xa - xb
+        d -= s.box * np.round(d / s.box)
+        print(r, "max|dlam|", np.abs(la - lb).max(), "max|dx|", np.abs(d).max())
+        assert np.abs(la - lb).max() < 1e-5 and np.abs(d).max() < 1e-4
+    # a single-replica restore must not move the shared clock
+    c = mk()
+    with pytest.raises(cph.CphError) as ei:
+        c.cph_set_state(0, a.cph_get_state(0))
+    assert ei.value.status == 4

@@ -502,3 +502,15 @@ def test_pfc_saturates_when_target_unreachable():
     w = np.exp(-(V - V.min()) / kT(300.0))
     frac = w[x >= 0.5].sum() / w.sum()
     assert frac < 1e-3 and 1.0 / (10 ** 5 + 1) < frac
+
+
+def test_canonical_partner_rows_equal_the_pair_list():
+    """oracle.pairlist.canonical_partners (sampled rows for large systems) gives exactly the
+    rows of canonical_pairs (both orientations of every pair, bit-identical d2)."""
+    s = small_system()
+    pairs = pairlist.canonical_pairs(s.pos, s.box, 1.1, s.excl)
+    idx = np.arange(0, s.n_atoms, 7)
+    rows = pairlist.canonical_partners(s.pos, s.box, 1.1, s.excl, idx)
+    for i, row in zip(idx, rows):
+        ref = np.sort(np.concatenate([pairs[pairs[:, 0] == i, 1], pairs[pairs[:, 1] == i, 0]]))
+        assert np.array_equal(row, ref)
