@@ -164,3 +164,93 @@ def bootstrap(pH_levels, fractions, B=5000, seed=0, hill=False):
             continue
     d = np.asarray(draws)
     return est, np.percentile(d, 2.5, axis=0), np.percentile(d, 97.5, axis=0)
+
+
+# ---- residue-residue coupling screen -----------------
+def binary_protonation(lambda_p_frames):
+    """Binary protonation trajectory: 1 = protonated (lambda_p < 0.5), 0 = deprotonated
+    (reading R1)."""
+    return (np.asarray(lambda_p_frames, np.float64) < 0.5).astype(np.int8)
+
+
+def _entropy(p):
+    p = p[p > 0]
+    return float(-(p * np.log(p)).sum())      # H = -sum p ln p (PAPER.md:1029, sign restored)
+
+
+def nmi(x, y):
+    """Normalised mutual information of two binary trajectories (same frames):
+    NMI = 2 I(X;Y) / (H(X) + H(Y)), natural logs; 0 when both are constant.
+    Returns (NMI, H(X), H(Y))."""
+    x = np.asarray(x).astype(np.int64).ravel()
+    y = np.asarray(y).astype(np.int64).ravel()
+    if x.shape != y.shape or x.size == 0:
+        raise ValueError("need two non-empty trajectories of equal length")
+    joint = np.bincount(2 * x + y, minlength=4).reshape(2, 2) / x.size
+    px, py = joint.sum(1), joint.sum(0)
+    hx, hy, hxy = _entropy(px), _entropy(py), _entropy(joint.ravel())
+    mi = hx + hy - hxy
+    return (2.0 * mi / (hx + hy) if hx + hy > 0 else 0.0), hx, hy
+
+
+def coupling_screen(frames, threshold=0.1):
+    """frames [n_pH, R, F, S]: lambda_p of S sites, F frames, R replicas, n_pH points.
+    For every site pair: NMI and entropies per replica and pH point, averaged over replicas;
+    a pair is coupled when, at any pH point, the mean NMI and both mean entropies exceed the
+    threshold (0.1).  Returns (coupled pairs [(a, b)], mean NMI
+    [n_pH, S, S], mean H [n_pH, S])."""
+    f = np.asarray(frames, np.float64)
+    npH, R, F, S = f.shape
+    b = binary_protonation(f)
+    m_nmi = np.zeros((npH, S, S))
+    m_h = np.zeros((npH, S))
+    for k in range(npH):
+        for r in range(R):
+            for a in range(S):
+                for c in range(a + 1, S):
+                    v, ha, hc = nmi(b[k, r, :, a], b[k, r, :, c])
+                    m_nmi[k, a, c] += v / R
+                    m_nmi[k, c, a] += v / R
+            m_h[k] += np.array([_entropy(np.bincount(b[k, r, :, a], minlength=2) / F) for a in range(S)]) / R
+    coupled = [(a, c) for a in range(S) for c in range(a + 1, S)
+               if np.any((m_nmi[:, a, c] > threshold) & (m_h[:, a] > threshold) & (m_h[:, c] > threshold))]
+    return coupled, m_nmi, m_h
+
+
+def two_site_protons(pH, pKa1, pKa2):
+    """Macroscopic titration of two interacting sites: mean number of bound protons
+    <X> = (10^(pKa2-pH) + 2 10^(pKa1+pKa2-2pH)) / (1 + 10^(pKa2-pH) + 10^(pKa1+pKa2-2pH))
+    (PAPER.md:1014-1016)."""
+    pH = np.asarray(pH, np.float64)
+    a = np.power(10.0, pKa2 - pH)
+    b = np.power(10.0, pKa1 + pKa2 - 2.0 * pH)
+    return (a + 2.0 * b) / (1.0 + a + b)
+
+
+def fit_two_site(pH, protons, iters=200):
+    """Least squares of two_site_protons to <X> per pH (and replica) by Levenberg-Marquardt
+    with a numerical Jacobian.  Returns (pKa1, pKa2)."""
+    pH = np.asarray(pH, np.float64)
+    y = np.asarray(protons, np.float64)
+    mid = pH[np.argmin(np.abs(y - 1.0))]
+    p = np.array([mid - 1.0, mid + 1.0])
+    mu = 1e-3
+
+    def resid(v):
+        return two_site_protons(pH, v[0], v[1]) - y
+    r = resid(p)
+    for _ in range(iters):
+        J = np.stack([(resid(p + e) - resid(p - e)) / 2e-7 for e in (np.array([1e-7, 0.0]), np.array([0.0, 1e-7]))], 1)
+        A = J.T @ J
+        step = np.linalg.solve(A + mu * np.diag(np.diag(A) + 1e-30), -(J.T @ r))
+        rt = resid(p + step)
+        if rt @ rt < r @ r:
+            p, r = p + step, rt
+            mu = max(mu * 0.3, 1e-12)
+            if np.max(np.abs(step)) < 1e-12:
+                break
+        else:
+            mu *= 10.0
+            if mu > 1e12:
+                break
+    return float(p[0]), float(p[1])
