@@ -325,7 +325,9 @@ def main():
     ctx.cph_sync()
     alg = algorithmic(s, R)
     hbm, hbm_kind = peaks()
-    per = {k: (prof_ms[k] / prof_n[k] if prof_n.get(k) else (prof_ms[k] / args.profile_steps)) for k in prof_ms}
+    # cuFFT executions are not counted by the library (one R2C and one C2R plan execution per step)
+    execs = {k: (prof_n[k] if prof_n.get(k) else (args.profile_steps if k.startswith("fft") else 0)) for k in prof_ms}
+    per = {k: prof_ms[k] / execs[k] for k in prof_ms if execs[k]}
     total_prof = sum(prof_ms.values())
     kernels = {}
     work = {"nonbonded": ("alu", alg["nonbonded_flop"], "TFLOP/s"), "spread": ("hbm", alg["spread_bytes"], "GB/s"),
@@ -333,9 +335,7 @@ def main():
             "fft_r2c": ("hbm", alg["fft_bytes_each"], "GB/s"), "fft_c2r": ("hbm", alg["fft_bytes_each"], "GB/s"),
             "integrate": ("hbm", alg["integrate_bytes"], "GB/s")}
     for k, t_ms in per.items():
-        if not prof_n.get(k):
-            continue
-        ent = {"ms_per_launch": t_ms, "launches_per_step": prof_n[k] / args.profile_steps,
+        ent = {"ms_per_launch": t_ms, "launches_per_step": execs[k] / args.profile_steps,
                "share_of_step": prof_ms[k] / total_prof if total_prof else None}
         if k in work and t_ms > 0:
             bound, amount, unit = work[k]
@@ -345,6 +345,9 @@ def main():
             else:
                 ach = amount / (t_ms * 1e-3) / 1e9
                 ent.update(bound=bound, achieved=ach, unit=unit, frac=ach / hbm)
+        if k == "pairlist":
+            rebuilds = max(1, args.profile_steps // int(s.params["nstlist"]))
+            ent["ms_per_rebuild"] = prof_ms[k] / rebuilds
         kernels[k] = ent
     ours = [k for k in kernels if not k.startswith("fft")]
     dom = max(ours, key=lambda k: prof_ms[k])

@@ -65,5 +65,5 @@ def deprotonated_fraction(pKa, pH, T, h, kw, b=0.0, c=0.0, vmm=None, n=400001):
     return float(np.trapezoid(wd, dx=dx) / np.trapezoid(w, dx=dx))
 
 
-def titration_curve(pKa, pH_levels, T, h, kw, b=0.0, c=0.0, vmm=None):
-    return np.array([deprotonated_fraction(pKa, p, T, h, kw, b, c, vmm) for p in pH_levels])
+def titration_curve(pKa, pH_levels, T, h, kw, b=0.0, c=0.0, vmm=None, n=400001):
+    return np.array([deprotonated_fraction(pKa, p, T, h, kw, b, c, vmm, n) for p in pH_levels])

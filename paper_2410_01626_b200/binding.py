@@ -382,9 +382,8 @@ class Context:
         assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and t.numel() >= self.R * (self.P + 1)
         cur, ls = torch.cuda.current_stream(t.device), self.lib_stream()
         ls.wait_stream(cur)
-        t.record_stream(ls)
         self.cph_exchange_energies(t.data_ptr())
-        cur.wait_stream(ls)
+        cur.wait_stream(ls)      # later use or reuse of t on torch's stream follows the write
 
     def exchange_apply_from(self, t, seed, attempt):
         """Apply the decisions from the gathered rows t (filled on torch's current stream)."""
@@ -392,9 +391,8 @@ class Context:
         assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
         cur, ls = torch.cuda.current_stream(t.device), self.lib_stream()
         ls.wait_stream(cur)
-        t.record_stream(ls)
         self.cph_exchange_apply(t.data_ptr(), seed, attempt)
-        cur.wait_stream(ls)
+        cur.wait_stream(ls)      # the caching allocator may reuse t only after this read
 
     def cph_get_labels(self):
         lab = np.zeros(self.R, np.int32)

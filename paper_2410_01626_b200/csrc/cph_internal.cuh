@@ -45,6 +45,7 @@ struct KParams {
   // cells
   int nc[3], ncell;            // cells per dimension, total
   int ns[3], so[3];            // stencil sizes and first offsets per dimension
+  int nb_packed;               // pair kernel: FFMA2 path for non-lambda warps (A/B: CPH_NB_PACKED=0)
   // list
   int cap;                     // neighbour capacity per atom
   // PME

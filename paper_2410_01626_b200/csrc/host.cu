@@ -651,6 +651,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     else { kp.ns[d] = nc; kp.so[d] = 0; }
     kp.ncell *= nc;
   }
+  kp.nb_packed = getenv("CPH_NB_PACKED") ? atoi(getenv("CPH_NB_PACKED")) : 1;
   {
     const double expect = (double)N / V * 4.0 / 3.0 * kPi * std::pow(prm->rlist, 3);
     kp.cap = (int)std::ceil(1.6 * expect + 64.0);

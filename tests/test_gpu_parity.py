@@ -450,3 +450,24 @@ def test_checkpoint_restore_continues_the_run(cph):
     with pytest.raises(cph.CphError) as ei:
         c.cph_set_state(0, a.cph_get_state(0))
     assert ei.value.status == 4
+
+
+def test_packed_pair_path_matches_scalar_path(cph, monkeypatch):
+    """The FFMA2 pair path (non-lambda warps and lambda warps between energy steps) against
+    the scalar path that every snapshot test checks against the oracle: two contexts, one
+    with CPH_NB_PACKED=0, stepped through non-energy steps (nstenergy = 1000) with the same
+    noise; positions and lambdas agree to fp32 rounding growth."""
+    s = make_system(2)
+    ctxs = []
+    for packed in ("1", "0"):
+        monkeypatch.setenv("CPH_NB_PACKED", packed)
+        ctxs.append(_ctx(cph, s, 3, seed=8, nstenergy=1000)[0])
+    for c in ctxs:
+        c.cph_step(9)                      # steps 1..8 are not energy steps: packed path
+    for r in range(3):
+        xa, xb = ctxs[0].cph_get_positions(r)[0], ctxs[1].cph_get_positions(r)[0]
+        la, lb = ctxs[0].cph_get_lambdas(r)[0], ctxs[1].cph_get_lambdas(r)[0]
+        d = xa - xb
+        d -= s.box * np.round(d / s.box)
+        print(r, "max|dx|", np.abs(d).max(), "max|dlam|", np.abs(la - lb).max())
+        assert np.abs(d).max() < 2e-5 and np.abs(la - lb).max() < 2e-6

@@ -32,9 +32,9 @@ def test_linear_coulomb_term_shifts_pka_by_about_b_over_ln10kT():
     """A linear Coulomb term b lambda adds to the pH term (which the PFC, computed from
     Vdw + VpH only, does not see): the fitted pKa moves by ~ b/(ln10 kT) (the PFC depth,
     tuned for the unshifted pH term, makes it inexact), in the direction of b's sign."""
-    pH = np.linspace(2.5, 6.5, 17)
+    pH = np.linspace(2.5, 6.5, 9)
     for b in (-4.0, 4.0):
-        x = TQ.titration_curve(4.4, pH, 300.0, 2.0, 1e6, b=b)
+        x = TQ.titration_curve(4.4, pH, 300.0, 2.0, 1e6, b=b, n=100001)
         shift = analysis.fit_hh(pH, x) - 4.4
         expect = b / (math.log(10.0) * kT(300.0))
         assert np.sign(shift) == np.sign(expect) and abs(shift - expect) < 0.4 * abs(expect), (shift, expect)
@@ -56,7 +56,7 @@ def test_coulomb_quadratic_matches_engine_dvdl():
 def test_quadrature_matches_oracle_lambda_dynamics():
     """The same 1-D potential sampled by oracle.lambda_only (linear + quadratic Coulomb
     term supplied through V_mm's c_10, c_20)."""
-    pKa, h, M = 4.4, 2.0, 1500
+    pKa, h, M = 4.4, 2.0, 1000
     b, c = -3.0, 2.5
     pHs = np.array([3.9, 4.7])
     vmm = np.zeros(36)
@@ -68,7 +68,7 @@ def test_quadrature_matches_oracle_lambda_dynamics():
     seeds = np.arange(1, 2 * M + 1, dtype=np.uint64) * np.uint64(40503) + np.uint64(11)
     # a light lambda particle (the mass does not enter the equilibrium density) relaxes in
     # ~1 ps, so the start (half at 0, half at 1) is forgotten after the first 4 ps
-    fr, _ = run_2state(seeds, lam0, pKa, pH, 6000, h_barrier=h, d1=d1, vmm=vmm, mass=6.0)
-    fr = fr[200:]
+    fr, _ = run_2state(seeds, lam0, pKa, pH, 4000, h_barrier=h, d1=d1, vmm=vmm, mass=6.0)
+    fr = fr[150:]
     x = np.array([analysis.deprotonated_fraction(fr[:, k * M:(k + 1) * M]) for k in range(2)])
-    assert np.all(np.abs(x - ref) < 0.015), (x, ref)
+    assert np.all(np.abs(x - ref) < 0.02), (x, ref)
