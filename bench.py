@@ -339,6 +339,7 @@ def main():
                "share_of_step": prof_ms[k] / total_prof if total_prof else None}
         if k in work and t_ms > 0:
             bound, amount, unit = work[k]
+            t_ms = prof_ms[k] / args.profile_steps            # the class's device time per step
             if unit == "TFLOP/s":
                 ach = amount / (t_ms * 1e-3) / 1e12
                 ent.update(bound=bound, achieved=ach, unit=unit, frac=ach / FP32_PEAK_TFLOPS)

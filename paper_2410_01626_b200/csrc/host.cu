@@ -1776,7 +1776,7 @@ cph_status cph_profile_steps(cph_ctx *ctx, int64_t n_steps, double *ms, int64_t 
     const bool rebuild = (c.host_step + 1) % c.kp.nstlist == 0;
     { int q = launch_integrate(c, s, 1); k += q; cnt[CPH_K_INTEGRATE] += q; mark(CPH_K_INTEGRATE); }
     if (rebuild) { int q = launch_rebuild(c, s); k += q; cnt[CPH_K_PAIRLIST] += q; mark(CPH_K_PAIRLIST); }
-    k += launch_nonbonded(c, s, 1); cnt[CPH_K_NONBONDED] += 1; mark(CPH_K_NONBONDED);
+    { int q = launch_nonbonded(c, s, 1); k += q; cnt[CPH_K_NONBONDED] += q; mark(CPH_K_NONBONDED); }
     k += launch_spread(c, s); cnt[CPH_K_SPREAD] += 1; mark(CPH_K_SPREAD);
     cufftExecR2C(c.plan_r2c, c.d.grid, (cufftComplex *)c.d.cgrid); mark(CPH_K_FFT_R2C);
     k += launch_solve(c, s, 1); cnt[CPH_K_SOLVE] += 1; mark(CPH_K_SOLVE);

@@ -12,6 +12,9 @@
 // Warps that contain a lambda atom also accumulate phi in fp64 (dV/dlambda at 2e-5; BASELINE
 // "fp64 lambda reductions"); on energy steps the per-atom sums are fp64 as well.
 // Compiled with -ftz=true: no denormal fix-ups around MUFU.RSQ / RCP / EX2.
+#include <algorithm>
+#include <cstdlib>
+
 #include "cph_device.cuh"
 
 namespace cph {
@@ -272,7 +275,7 @@ __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, 
   }
 }
 
-__global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevBufs d, int step_offset) {
+__global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevBufs d, int step_offset, int r0) {
   // LJ tables sized T*T (dynamic shared memory): the rest of the SM's 256 KB stays L1 cache
   // for the neighbour-position gathers
   extern __shared__ float2 s_lj[];
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevB
     s_shn[code] = make_float4(-s_shift[code].x, -s_shift[code].y, -s_shift[code].z, 0.f);
   }
   __syncthreads();
-  const int r = blockIdx.y;
+  const int r = r0 + blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < kp.N;
   const long long m = *d.step + step_offset;
@@ -330,7 +333,7 @@ __global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevB
 
 int launch_nonbonded(Ctx &c, cudaStream_t s, int step_offset) {
   dim3 grid((c.kp.N + 127) / 128, c.kp.R);
-  k_nonbonded<<<grid, 128, 3 * sizeof(float2) * c.kp.T * c.kp.T, s>>>(c.kp, c.d, step_offset);
+  k_nonbonded<<<grid, 128, 3 * sizeof(float2) * c.kp.T * c.kp.T, s>>>(c.kp, c.d, step_offset, 0);
   return 1;
 }
 
