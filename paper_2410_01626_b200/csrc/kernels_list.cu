@@ -9,8 +9,6 @@
 // bit-exact against the oracle's.  Entries: sorted slot (21 bits) | LJ type (5 bits) | image
 // code (5 bits); stored in 8-entry tiles nbl[k/8][i][k%8] so the builder writes whole 32-byte
 // sectors per lane and a warp of the pair kernel reads 1 KB contiguous per 8 neighbours.
-#include <cstdlib>
-
 #include "cph_device.cuh"
 
 namespace cph {
@@ -412,267 +410,6 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
   }
 }
 
-__global__ void __launch_bounds__(32) k_build_list_bf(KParams kp, DevBufs d) {
-  const int r = blockIdx.y, c = blockIdx.x;
-  const int lane = threadIdx.x;
-  const size_t base = (size_t)r * kp.Nst;
-  const float4 *xq = d.xyzq + base;
-  const int2 *meta = d.meta + base;
-  const int *start = d.cell_start + (size_t)r * (kp.ncell + 1);
-  __shared__ float4 sx[32];
-  __shared__ int sj[32];
-  __shared__ uint32_t s_buf[16][32];
-  const int cz = c % kp.nc[2], cy = (c / kp.nc[2]) % kp.nc[1], cx = c / (kp.nc[2] * kp.nc[1]);
-  const int ib = start[c], ie = start[c + 1];
-  const float3 Lbox = make_float3(kp.L[0], kp.L[1], kp.L[2]);
-  const float3 Linv = make_float3(kp.invL[0], kp.invL[1], kp.invL[2]);
-  const float rlist2 = kp.rlist2;
-  // band around r_list^2 inside which the fast (image-staged, rounding-different) d^2 may
-  // disagree with the canonical fp32 value; |delta d^2| < 1e-5 r_list^2 (R14)
-  const float lo2 = kp.rlist2 * (1.0f - 3e-5f), hi2 = kp.rlist2 * (1.0f + 3e-5f);
-  const bool fast = kp.ns[0] == 5 && kp.ns[1] == 5 && kp.ns[2] == 5;
-  const float csx = kp.L[0] / (float)kp.nc[0], csy = kp.L[1] / (float)kp.nc[1], csz = kp.L[2] / (float)kp.nc[2];
-  const float win_r = sqrtf(kp.rlist2) * 1.0001f + kWinPad;
-  const float win_r2 = win_r * win_r;
-  // stencil tables (cell index and, for +-2 stencils, the uniform periodic image shift
-  // L * floor(raw / nc) of that j-cell; dimensions with < 5 cells use per-lane images)
-  __shared__ int s_cell[3][8];
-  __shared__ float s_wsh[3][8];
-  __shared__ int s_wi[3][8];
-  if (lane < 24) {
-    const int dd = lane >> 3, o = lane & 7;
-    const int cdim = dd == 0 ? cx : (dd == 1 ? cy : cz);
-    if (o < kp.ns[dd]) {
-      const int raw = cdim + kp.so[dd] + o;
-      const int w = kp.ns[dd] == 5 ? (raw + kp.nc[dd]) / kp.nc[dd] - 1 : 0;
-      s_cell[dd][o] = (raw + 2 * kp.nc[dd]) % kp.nc[dd];
-      s_wi[dd][o] = w;
-      s_wsh[dd][o] = kp.L[dd] * (float)w;
-    }
-  }
-  __syncwarp();
-  // [start, end) of every stencil cell, in the walk order (ox, oy, oz)
-  __shared__ int s_jb[125], s_je[125];
-  {
-    const int nyz = kp.ns[1] * kp.ns[2], nst = kp.ns[0] * nyz;
-    for (int t = lane; t < nst; t += 32) {
-      const int w = fast ? c_walk[t] : t;
-      const int ox = w / nyz, oy = (w / kp.ns[2]) % kp.ns[1], oz = w % kp.ns[2];
-      const int cc = (s_cell[0][ox] * kp.nc[1] + s_cell[1][oy]) * kp.nc[2] + s_cell[2][oz];
-      s_jb[t] = start[cc];
-      s_je[t] = start[cc + 1];
-    }
-  }
-  __syncwarp();
-  for (int i0 = ib; i0 < ie; i0 += 32) {
-    const int i = i0 + lane;
-    const bool valid = i < ie;
-    const float4 xi = valid ? xq[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const int orig = valid ? meta[i].x : 0;
-    const int eb = valid ? d.excl_ptr[orig] : 0, ee = valid ? d.excl_ptr[orig + 1] : 0;
-    const bool any_solute = __any_sync(0xffffffffu, ee > eb);
-    // list tile layout: entries k of atom i at nbl[r][k / 8][i][k % 8]; each lane
-    // collects 8 entries in its shared-memory column and writes them as one 32-byte sector
-    uint4 *out = reinterpret_cast<uint4 *>(d.nbl + (size_t)r * kp.cap * kp.Nst) + 2 * (size_t)(valid ? i : 0);
-    const size_t ostride = 2 * (size_t)kp.Nst;                 // uint4 per 8-entry block row
-    int cnt = 0, flushed = 0;
-    // Flat walk over the stencil cells (ox, oy, oz).  Cell ranges come from shared memory
-    // and the next cell's first chunk of positions is loaded while the current one is
-    // tested, so the warp waits for one memory latency per rebuild instead of two per cell.
-    const int nyz = kp.ns[1] * kp.ns[2], nst = kp.ns[0] * nyz;
-    float4 pc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int tc = 0;
-    {
-      const int jb = s_jb[0];
-      if (lane < s_je[0] - jb) { pc = xq[jb + lane]; tc = meta[jb + lane].y; }
-    }
-    float zlo = -INFINITY, zhi = INFINITY;
-    for (int t = 0; t < nst; ++t) {
-      float4 pn = make_float4(0.f, 0.f, 0.f, 0.f);
-      int tn = 0;
-      if (t + 1 < nst) {
-        const int jb = s_jb[t + 1];
-        if (lane < s_je[t + 1] - jb) { pn = xq[jb + lane]; tn = meta[jb + lane].y; }
-      }
-      const int w = fast ? c_walk[t] : t;
-      const int ox = w / nyz, oy = (w / kp.ns[2]) % kp.ns[1], oz = w % kp.ns[2];
-      const float wsx = s_wsh[0][ox], wsy = s_wsh[1][oy], wsz = s_wsh[2][oz];
-      bool skip = false;
-      if (fast) {
-        if (t % 5 == 0) {                // first cell of a column in the walk
-          // z window of this stencil column.  Each lane's reach in z is sqrt(R^2 - dxy^2), dxy
-          // its xy distance to the column (geometric cell bounds in the staged image frame,
-          // padded); the warp tests only the staged atoms whose z lies in the union of the
-          // lanes' windows (cells are z-sorted, so that is a contiguous slice).  R and the pads
-          // are far outside the fp32 rounding of d^2, so no accepted pair is cut.
-          const float xlo = (float)(cx - 2 + ox) * csx - kWinPad, xhi = xlo + csx + 2.f * kWinPad;
-          const float ylo = (float)(cy - 2 + oy) * csy - kWinPad, yhi = ylo + csy + 2.f * kWinPad;
-          const float ddx = fmaxf(0.f, fmaxf(xlo - xi.x, xi.x - xhi));
-          const float ddy = fmaxf(0.f, fmaxf(ylo - xi.y, xi.y - yhi));
-          const float rr2 = win_r2 - ddx * ddx - ddy * ddy;
-          zlo = INFINITY; zhi = -INFINITY;
-          if (valid && rr2 > 0.f) {
-            const float rr = sqrtf(rr2);
-            zlo = xi.z - rr; zhi = xi.z + rr;
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
-            zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
-          }
-        }
-        const float zc = (float)(cz - 2 + oz) * csz;
-        skip = !(zlo <= zhi) || zhi < zc - kWinPad || zlo > zc + csz + kWinPad;
-      }
-      // accepted pairs' canonical image k = -(j-cell shift) (nearest image, r < L/2)
-      const int fast_code = (1 - s_wi[0][ox]) * 9 + (1 - s_wi[1][oy]) * 3 + (1 - s_wi[2][oz]);
-      const int jb = s_jb[t], je = s_je[t];
-      for (int j0 = jb; !skip && j0 < je; j0 += 32) {
-        const int nj = min(32, je - j0);
-        int tb = 0, te = nj;
-        float4 p = pc;
-        int ty = tc;
-        if (j0 != jb && lane < nj) { p = xq[j0 + lane]; ty = meta[j0 + lane].y; }   // cells > 32 atoms
-        __syncwarp();
-        {
-          float zt = 0.f;
-          if (lane < nj) {
-            // fast path: stage the j-cell's periodic image (uniform for a +-2 stencil)
-            sx[lane] = fast ? make_float4(p.x + wsx, p.y + wsy, p.z + wsz, 0.f) : p;
-            sj[lane] = (j0 + lane) | ((ty & (int)kEntryTypeMask) << kEntryTypeShift);
-            zt = p.z + wsz;
-          }
-          if (fast) {
-            tb = __popc(__ballot_sync(0xffffffffu, lane < nj && zt < zlo));
-            te = __popc(__ballot_sync(0xffffffffu, lane < nj && zt <= zhi));
-          }
-        }
-        __syncwarp();
-        if (fast) {
-          // Branch-free accept path: every lane tests the staged candidates, stores the entry
-          // word into its ring slot unconditionally and advances its count only on accept, so
-          // the warp never diverges on the ~28 % acceptance; the exact canonical decision
-          // (rounding band) and the exclusion scan (solute lanes) run only when some lane
-          // needs them.
-          const uint32_t code_bits = (uint32_t)fast_code << kEntryImgShift;
-          for (int t0 = tb; t0 < te; t0 += 4) {
-            float d2v[4];
-            uint32_t ej[4];
-            bool acc[4];
-            bool band = false;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int tt = min(t0 + u, te - 1);
-              const float4 xj = sx[tt];
-              ej[u] = (uint32_t)sj[tt];
-              const float dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
-              d2v[u] = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-              const bool inr = valid && t0 + u < te;
-              acc[u] = inr && d2v[u] < lo2;
-              band |= inr && d2v[u] >= lo2 && d2v[u] < hi2;
-            }
-            if (__any_sync(0xffffffffu, band)) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (valid && t0 + u < te && d2v[u] >= lo2 && d2v[u] < hi2)
-                  acc[u] = canonical_in(xq[ej[u] & kEntryJMask], xi, Lbox, Linv, rlist2);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u] = acc[u] && (int)(ej[u] & kEntryJMask) != i;
-            if (any_solute) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (acc[u] && ee > eb) {              // solute atoms only
-                  const int oj = meta[ej[u] & kEntryJMask].x;
-                  for (int e = eb; e < ee; ++e) acc[u] = acc[u] && d.excl_idx[e] != oj;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              s_buf[cnt & 15][lane] = ej[u] | code_bits;
-              cnt += acc[u] ? 1 : 0;
-            }
-            if (cnt - flushed >= 8) {
-              if (flushed < kp.cap) {
-                const int h = flushed & 8;
-                out[0] = make_uint4(s_buf[h][lane], s_buf[h + 1][lane], s_buf[h + 2][lane], s_buf[h + 3][lane]);
-                out[1] = make_uint4(s_buf[h + 4][lane], s_buf[h + 5][lane], s_buf[h + 6][lane], s_buf[h + 7][lane]);
-                out += ostride;
-              }
-              flushed += 8;
-            }
-          }
-          continue;
-        }
-        if (!valid) continue;
-        for (int t0 = tb; t0 < te; t0 += 4) {
-          float d2v[4], kxv[4], kyv[4], kzv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float4 xj = sx[min(t0 + u, te - 1)];
-            // canonical formula (R14): dx = x_j - x_i ; dx -= L rint(dx / L);
-            // positions are wrapped into [0, L] at the rebuild, so |dx / L| <= 1 and
-            // rint(t) == (t > 0.5) - (t < -0.5) exactly (ties to even)
-            const float rx = __fsub_rn(xj.x, xi.x), ry = __fsub_rn(xj.y, xi.y), rz = __fsub_rn(xj.z, xi.z);
-            kxv[u] = rint_unit(__fmul_rn(rx, Linv.x));
-            kyv[u] = rint_unit(__fmul_rn(ry, Linv.y));
-            kzv[u] = rint_unit(__fmul_rn(rz, Linv.z));
-            const float dx = __fsub_rn(rx, __fmul_rn(Lbox.x, kxv[u]));
-            const float dy = __fsub_rn(ry, __fmul_rn(Lbox.y, kyv[u]));
-            const float dz = __fsub_rn(rz, __fmul_rn(Lbox.z, kzv[u]));
-            d2v[u] = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
-          }
-          // small boxes (< 5 cells in some dimension): per-lane images, divergent appends
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (t0 + u >= te) continue;
-            if (!(d2v[u] < rlist2)) continue;
-            const int code = (int)(kxv[u] * 9.0f + kyv[u] * 3.0f + kzv[u]) + 13;
-            const int je_ = sj[t0 + u] | (code << kEntryImgShift);
-            const int j = je_ & (int)kEntryJMask;
-            if (j == i) continue;
-            if (ee > eb) {                    // solute atoms only
-              const int oj = meta[j].x;
-              bool ex = false;
-              for (int e = eb; e < ee; ++e) ex |= (d.excl_idx[e] == oj);
-              if (ex) continue;
-            }
-            s_buf[cnt & 15][lane] = (uint32_t)je_;
-            ++cnt;
-          }
-          if (cnt - flushed >= 8) {
-            if (flushed < kp.cap) {
-              const int h = flushed & 8;
-              out[0] = make_uint4(s_buf[h][lane], s_buf[h + 1][lane], s_buf[h + 2][lane], s_buf[h + 3][lane]);
-              out[1] = make_uint4(s_buf[h + 4][lane], s_buf[h + 5][lane], s_buf[h + 6][lane], s_buf[h + 7][lane]);
-              out += ostride;
-            }
-            flushed += 8;
-          }
-        }
-      }
-      pc = pn;
-      tc = tn;
-    }
-    if (valid && cnt > flushed && flushed < kp.cap) {
-      // pad the last tile with the atom's own slot (zero shift, r = 0: skipped by the pair kernel)
-      const uint32_t self = (uint32_t)i | ((uint32_t)(meta[i].y & (int)kEntryTypeMask) << kEntryTypeShift) |
-                            (13u << kEntryImgShift);
-      const int h = flushed & 8;
-      for (int k = cnt - flushed; k < 8; ++k) s_buf[h + k][lane] = self;
-      out[0] = make_uint4(s_buf[h][lane], s_buf[h + 1][lane], s_buf[h + 2][lane], s_buf[h + 3][lane]);
-      out[1] = make_uint4(s_buf[h + 4][lane], s_buf[h + 5][lane], s_buf[h + 6][lane], s_buf[h + 7][lane]);
-    }
-    if (valid) {
-      d.nnb[base + i] = cnt;
-      if (cnt > kp.cap) {
-        d.flags[FLAG_LIST_OVERFLOW] = 1;
-        atomicMax(&d.flags[FLAG_MAX_NNB], cnt);
-      }
-    }
-  }
-}
-
 // spatial sort + permutation of every per-atom array (positions wrapped); the pair list
 // itself is launch_build_list, so work that only needs the new atom order (the PME chain) can
 // start while the list is built
@@ -690,9 +427,7 @@ int launch_sort(Ctx &c, cudaStream_t s) {
 }
 
 int launch_build_list(Ctx &c, cudaStream_t s) {
-  static const bool bf = getenv("CPH_BUILD_BF") != nullptr;     // A/B: branch-free accept path
-  if (bf) k_build_list_bf<<<dim3(c.kp.ncell, c.kp.R), 32, 0, s>>>(c.kp, c.d);
-  else k_build_list<<<dim3(c.kp.ncell, c.kp.R), 32, 0, s>>>(c.kp, c.d);
+  k_build_list<<<dim3(c.kp.ncell, c.kp.R), 32, 0, s>>>(c.kp, c.d);
   return 1;
 }
 
