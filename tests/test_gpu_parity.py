@@ -471,3 +471,29 @@ def test_packed_pair_path_matches_scalar_path(cph, monkeypatch):
         d -= s.box * np.round(d / s.box)
         print(r, "max|dx|", np.abs(d).max(), "max|dlam|", np.abs(la - lb).max())
         assert np.abs(d).max() < 2e-5 and np.abs(la - lb).max() < 2e-6
+
+
+def test_c1_200_step_trajectory_diagnostic(cph):
+    """SURVEY §8(c) trajectory diagnostic: C1 (1.5k atoms, one Glu), same Philox streams, 200
+    steps, positions and lambda compared at steps 1, 10, 100 and 200.  fp32 (GPU) vs fp64
+    (oracle) differences grow with the chaotic dynamics; steps 1 and 10 are gated at the
+    snapshot level, 100 and 200 are reported with a loose sanity bound (reading A18)."""
+    s = make_system(1)
+    lam0 = np.array([[0.35]])
+    vel = make_velocities(s, 17)[None]
+    ctx = cph.cph_create(s, [4.4], [4242], lambda0=lam0, vel_replicas=vel)
+    ref = OracleReplica(s, 4.4, 4242, lam0=lam0[0], vel0=vel[0])
+    done = 0
+    for target, (tol_x, tol_l) in ((1, (1e-5, 1e-6)), (10, (1e-4, 1e-5)), (100, (2e-2, 2e-2)),
+                                   (200, (5e-2, 5e-2))):
+        ctx.cph_step(target - done)
+        while ref.step_index < target:
+            ref.step()
+        done = target
+        x, _ = ctx.cph_get_positions(0)
+        lam, _ = ctx.cph_get_lambdas(0)
+        d = x - ref.x
+        d -= s.box * np.round(d / s.box)
+        dx, dl = float(np.abs(d).max()), float(np.abs(lam - ref.lam).max())
+        print(f"step {target}: max|dx| {dx:.3e} nm, max|dlambda| {dl:.3e}")
+        assert dx < tol_x and dl < tol_l
