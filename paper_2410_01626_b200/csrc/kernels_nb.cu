@@ -149,7 +149,7 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
 // formulas and rounding as nb_atom (each packed op is the scalar op, element-wise).
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-template <bool PHI64>
+template <bool PHI64, bool SMALLT>
 __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, const float4 *__restrict__ xq,
                                            const float *__restrict__ c6n, const float *__restrict__ c12t,
                                            const float4 *__restrict__ shn, int r, int i, bool valid, float4 xi, int ti,
@@ -165,6 +165,21 @@ __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, 
   const uint4 *L = reinterpret_cast<const uint4 *>(d.nbl + (size_t)r * kp.cap * kp.Nst) + 2 * (size_t)i;
   const size_t tstride = 2 * (size_t)kp.Nst;
   const int lrow = ti * kp.T;
+  // T <= 4 LJ types (the synthetic systems): the lane's LJ row lives in registers and is
+  // selected with FSELs, so the pair loop issues no shared-memory load for it (the kernel is
+  // bound by LSU wavefronts: global gathers + shared loads)
+  float r6n[4] = {0.f, 0.f, 0.f, 0.f}, r12[4] = {0.f, 0.f, 0.f, 0.f};
+  if (SMALLT) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (t < kp.T) { r6n[t] = c6n[lrow + t]; r12[t] = c12t[lrow + t]; }
+  }
+  auto ljsel = [&](uint32_t e, float &v6, float &v12) {
+    const uint32_t t = (e >> kEntryTypeShift) & kEntryTypeMask;
+    const bool hi = t & 2u, od = t & 1u;
+    v6 = hi ? (od ? r6n[3] : r6n[2]) : (od ? r6n[1] : r6n[0]);
+    v12 = hi ? (od ? r12[3] : r12[2]) : (od ? r12[1] : r12[0]);
+  };
   const float rc2 = kp.rc2;
   const float kexp = -kp.beta * kp.beta * 1.4426950408889634f;
   const float2 kexp2 = f2(kexp, kexp);
@@ -183,9 +198,16 @@ __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, 
     const float4 xa = __ldg(reinterpret_cast<const float4 *>(xqb + (size_t)((ea & kEntryJMask) << 4)));
     const float4 xb = __ldg(reinterpret_cast<const float4 *>(xqb + (size_t)((eb & kEntryJMask) << 4)));
     const float4 sa = shn[ea >> kEntryImgShift], sb = shn[eb >> kEntryImgShift];
-    const int la = lrow + (int)((ea >> kEntryTypeShift) & kEntryTypeMask);
-    const int lb = lrow + (int)((eb >> kEntryTypeShift) & kEntryTypeMask);
-    const float2 c6 = f2(c6n[la], c6n[lb]), c12 = f2(c12t[la], c12t[lb]);   // (-6 c6, 12 c12)
+    float2 c6, c12;                                                        // (-6 c6, 12 c12)
+    if (SMALLT) {
+      ljsel(ea, c6.x, c12.x);
+      ljsel(eb, c6.y, c12.y);
+    } else {
+      const int la = lrow + (int)((ea >> kEntryTypeShift) & kEntryTypeMask);
+      const int lb = lrow + (int)((eb >> kEntryTypeShift) & kEntryTypeMask);
+      c6 = f2(c6n[la], c6n[lb]);
+      c12 = f2(c12t[la], c12t[lb]);
+    }
     const float2 da = __fadd2_rn(__fadd2_rn(f2(xa.x, xa.y), f2(sa.x, sa.y)), nxi);
     const float2 db = __fadd2_rn(__fadd2_rn(f2(xb.x, xb.y), f2(sb.x, sb.y)), nxi);
     const float dza = (xa.z + sa.z) + nzi, dzb = (xb.z + sb.z) + nzi;
@@ -316,11 +338,17 @@ __global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevB
   double elj = 0.0, ere = 0.0, eex = 0.0;
   if (warp_lam) {
     if (energy) nb_atom<true, true>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
-    else if (kNbPacked && kp.nb_packed) nb_atom_x2<true>(kp, d, xq, s_c6n, s_c12, s_shn, r, i, valid, xi, ti, lslot, n, nmax);
+    else if (kNbPacked && kp.nb_packed) {
+      if (kp.T <= 4) nb_atom_x2<true, true>(kp, d, xq, s_c6n, s_c12, s_shn, r, i, valid, xi, ti, lslot, n, nmax);
+      else nb_atom_x2<true, false>(kp, d, xq, s_c6n, s_c12, s_shn, r, i, valid, xi, ti, lslot, n, nmax);
+    }
     else nb_atom<false, true>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
   } else {
     if (energy) nb_atom<true, false>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
-    else if (kNbPacked && kp.nb_packed) nb_atom_x2<false>(kp, d, xq, s_c6n, s_c12, s_shn, r, i, valid, xi, ti, lslot, n, nmax);
+    else if (kNbPacked && kp.nb_packed) {
+      if (kp.T <= 4) nb_atom_x2<false, true>(kp, d, xq, s_c6n, s_c12, s_shn, r, i, valid, xi, ti, lslot, n, nmax);
+      else nb_atom_x2<false, false>(kp, d, xq, s_c6n, s_c12, s_shn, r, i, valid, xi, ti, lslot, n, nmax);
+    }
     else nb_atom<false, false>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
   }
   if (energy) {
