@@ -143,6 +143,12 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
   }
 }
 
+// -shift of the 27 image codes as a kernel parameter: indexed per entry it is read through the
+// constant cache (LDC), off the LSU data path that the neighbour gathers saturate
+struct ShiftTab {
+  float4 s[27];
+};
+
 // The hot path (no lambda atom in the warp, not an energy step) with the arithmetic of two
 // list entries packed into the sm_100 paired FP32 instructions (FFMA2 / FMUL2 / FADD2: one issue
 // slot for two lanes' worth of FP32 work); rsqrt / rcp / ex2 stay scalar on the MUFU pipe.  Same
@@ -152,7 +158,7 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 template <bool PHI64, bool SMALLT>
 __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, const float4 *__restrict__ xq,
                                            const float *__restrict__ c6n, const float *__restrict__ c12t,
-                                           const float4 *__restrict__ shn, int r, int i, bool valid, float4 xi, int ti,
+                                           const ShiftTab &shn, int r, int i, bool valid, float4 xi, int ti,
                                            int lslot, int n, int nmax) {
   // d_n = x_j - shift - x_i = -(x_i - x_j + shift): the packed adds need no negation; the force
   // sum is negated once at the end
@@ -197,7 +203,7 @@ __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, 
   auto pair = [&](uint32_t ea, uint32_t eb) {
     const float4 xa = __ldg(reinterpret_cast<const float4 *>(xqb + (size_t)((ea & kEntryJMask) << 4)));
     const float4 xb = __ldg(reinterpret_cast<const float4 *>(xqb + (size_t)((eb & kEntryJMask) << 4)));
-    const float4 sa = shn[ea >> kEntryImgShift], sb = shn[eb >> kEntryImgShift];
+    const float4 sa = shn.s[ea >> kEntryImgShift], sb = shn.s[eb >> kEntryImgShift];
     float2 c6, c12;                                                        // (-6 c6, 12 c12)
     if (SMALLT) {
       ljsel(ea, c6.x, c12.x);
@@ -297,7 +303,7 @@ __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, 
   }
 }
 
-__global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevBufs d, int step_offset, int r0) {
+__global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevBufs d, int step_offset, int r0, const ShiftTab shn) {
   // LJ tables sized T*T (dynamic shared memory): the rest of the SM's 256 KB stays L1 cache
   // for the neighbour-position gathers
   extern __shared__ float2 s_lj[];
@@ -306,7 +312,6 @@ __global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevB
   float *s_c6n = reinterpret_cast<float *>(s_lj + 2 * kp.T * kp.T);   // -6 c6 (packed path)
   float *s_c12 = s_c6n + kp.T * kp.T;                                  // 12 c12 (packed path)
   __shared__ float4 s_shift[27];                    // image shift L * (kx, ky, kz)
-  __shared__ float4 s_shn[27];                      // -shift (packed path)
   for (int t = threadIdx.x; t < kp.T * kp.T; t += blockDim.x) {
     const float2 c = d.ljtab[t];
     s_ljf[t] = c;
@@ -318,7 +323,6 @@ __global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevB
     const int code = threadIdx.x;
     s_shift[code] = make_float4(kp.L[0] * (float)(code / 9 - 1), kp.L[1] * (float)((code / 3) % 3 - 1),
                                 kp.L[2] * (float)(code % 3 - 1), 0.f);
-    s_shn[code] = make_float4(-s_shift[code].x, -s_shift[code].y, -s_shift[code].z, 0.f);
   }
   __syncthreads();
   const int r = r0 + blockIdx.y;
@@ -339,15 +343,15 @@ __global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevB
   if (warp_lam) {
     if (energy) nb_atom<true, true>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
     else if (kNbPacked && kp.nb_packed) {
-      if (kp.T <= 4) nb_atom_x2<true, true>(kp, d, xq, s_c6n, s_c12, s_shn, r, i, valid, xi, ti, lslot, n, nmax);
-      else nb_atom_x2<true, false>(kp, d, xq, s_c6n, s_c12, s_shn, r, i, valid, xi, ti, lslot, n, nmax);
+      if (kp.T <= 4) nb_atom_x2<true, true>(kp, d, xq, s_c6n, s_c12, shn, r, i, valid, xi, ti, lslot, n, nmax);
+      else nb_atom_x2<true, false>(kp, d, xq, s_c6n, s_c12, shn, r, i, valid, xi, ti, lslot, n, nmax);
     }
     else nb_atom<false, true>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
   } else {
     if (energy) nb_atom<true, false>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
     else if (kNbPacked && kp.nb_packed) {
-      if (kp.T <= 4) nb_atom_x2<false, true>(kp, d, xq, s_c6n, s_c12, s_shn, r, i, valid, xi, ti, lslot, n, nmax);
-      else nb_atom_x2<false, false>(kp, d, xq, s_c6n, s_c12, s_shn, r, i, valid, xi, ti, lslot, n, nmax);
+      if (kp.T <= 4) nb_atom_x2<false, true>(kp, d, xq, s_c6n, s_c12, shn, r, i, valid, xi, ti, lslot, n, nmax);
+      else nb_atom_x2<false, false>(kp, d, xq, s_c6n, s_c12, shn, r, i, valid, xi, ti, lslot, n, nmax);
     }
     else nb_atom<false, false>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
   }
@@ -361,7 +365,11 @@ __global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevB
 
 int launch_nonbonded(Ctx &c, cudaStream_t s, int step_offset) {
   dim3 grid((c.kp.N + 127) / 128, c.kp.R);
-  k_nonbonded<<<grid, 128, 3 * sizeof(float2) * c.kp.T * c.kp.T, s>>>(c.kp, c.d, step_offset, 0);
+  ShiftTab shn;
+  for (int code = 0; code < 27; ++code)
+    shn.s[code] = make_float4(-c.kp.L[0] * (float)(code / 9 - 1), -c.kp.L[1] * (float)((code / 3) % 3 - 1),
+                              -c.kp.L[2] * (float)(code % 3 - 1), 0.f);
+  k_nonbonded<<<grid, 128, 3 * sizeof(float2) * c.kp.T * c.kp.T, s>>>(c.kp, c.d, step_offset, 0, shn);
   return 1;
 }
 
