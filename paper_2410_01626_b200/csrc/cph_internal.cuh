@@ -95,6 +95,7 @@ struct DevBufs {
   float *grid = nullptr;                            // [R*K3]
   float2 *cgrid = nullptr;                          // [R*Kc]
   float *bsp = nullptr;                             // [Kx + Ky + Kz] |b|^2 moduli
+  float *ginf = nullptr;                            // [Kc] influence function G(m) (replica independent)
   int *g_kind = nullptr, *g_ptr = nullptr, *g_atoms = nullptr, *g_cptr = nullptr;
   double *g_q = nullptr;                            // [nlam*4]
   double *vmm = nullptr;                            // [G*36]
@@ -205,6 +206,7 @@ int launch_build_list(Ctx &c, cudaStream_t s);                     // pair list 
 int launch_nonbonded(Ctx &c, cudaStream_t s, int step_offset);
 int launch_spread(Ctx &c, cudaStream_t s);
 int launch_solve(Ctx &c, cudaStream_t s, int step_offset);
+int launch_influence(Ctx &c, cudaStream_t s);                      // G(m) table, once at create
 int launch_gather(Ctx &c, cudaStream_t s);
 int launch_lambda_reduce(Ctx &c, cudaStream_t s, int mode);       // 0 init eval, 1 step
 int launch_lambda_open(Ctx &c, cudaStream_t s);

@@ -787,6 +787,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   d.grid = dalloc<float>(c, (size_t)R * kp.K3);
   d.cgrid = dalloc<float2>(c, (size_t)R * kp.Kc);
   d.bsp = dalloc<float>(c, kp.K[0] + kp.K[1] + kp.K[2]);
+  d.ginf = dalloc<float>(c, kp.Kc);
   d.g_kind = dalloc<int>(c, G); d.g_ptr = dalloc<int>(c, G + 1);
   d.g_atoms = dalloc<int>(c, nlam); d.g_cptr = dalloc<int>(c, G + 1);
   d.g_q = dalloc<double>(c, 4 * (size_t)nlam);
@@ -947,6 +948,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     }
   }
   c.host_step = 0;
+  c.launches += launch_influence(c, c.stream);
   cph_status st = evaluate_here(c);
   if (st == CPH_OK) st = check_flags(c);
   // a denser-than-average region overflowed the list capacity: grow it once (with margin)

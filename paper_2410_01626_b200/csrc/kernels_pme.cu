@@ -70,7 +70,31 @@ __global__ void SPREAD_ATTR k_spread(KParams kp, DevBufs d) {
   }
 }
 
-// Qhat(m) *= G(m), G = exp(-pi^2 m^2/beta^2)/(pi V m^2) |b_x|^2 |b_y|^2 |b_z|^2 ; E_rec
+// Influence function G(m) = exp(-pi^2 m^2/beta^2)/(pi V m^2) |b_x|^2 |b_y|^2 |b_z|^2 on the
+// R2C half spectrum, G(0) = 0: identical for every replica (one box), so it is tabulated once
+// at create and the per-step solve is a streaming multiply.
+__global__ void __launch_bounds__(256) k_influence(KParams kp, DevBufs d) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= kp.Kc) return;
+  const int mz = idx % kp.Kzc;
+  const int t = idx / kp.Kzc;
+  const int my = t % kp.K[1];
+  const int mx = t / kp.K[1];
+  const float fx = (float)(mx <= kp.K[0] / 2 ? mx : mx - kp.K[0]) * kp.invL[0];
+  const float fy = (float)(my <= kp.K[1] / 2 ? my : my - kp.K[1]) * kp.invL[1];
+  const float fz = (float)mz * kp.invL[2];
+  const float m2 = fx * fx + fy * fy + fz * fz;
+  float G = 0.0f;
+  if (idx != 0) {
+    const float pi = 3.14159265358979f;
+    G = expf(-pi * pi * m2 / (kp.beta * kp.beta)) / (pi * kp.V * m2) * d.bsp[mx] * d.bsp[kp.K[0] + my] *
+        d.bsp[kp.K[0] + kp.K[1] + mz];
+  }
+  d.ginf[idx] = G;
+}
+
+// Qhat(m) *= G(m); E_rec = (f/2) sum_m G |Qhat|^2 with interior k_z planes of the half spectrum
+// weighted x2 (energy steps only)
 __global__ void __launch_bounds__(256) k_solve(KParams kp, DevBufs d, int step_offset) {
   const int r = blockIdx.y;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -78,23 +102,11 @@ __global__ void __launch_bounds__(256) k_solve(KParams kp, DevBufs d, int step_o
   const bool energy = is_energy_step(m, *d.end_step, kp.nstenergy);
   double e = 0.0;
   if (idx < kp.Kc) {
-    const int mz = idx % kp.Kzc;
-    const int t = idx / kp.Kzc;
-    const int my = t % kp.K[1];
-    const int mx = t / kp.K[1];
-    const float fx = (float)(mx <= kp.K[0] / 2 ? mx : mx - kp.K[0]) * kp.invL[0];
-    const float fy = (float)(my <= kp.K[1] / 2 ? my : my - kp.K[1]) * kp.invL[1];
-    const float fz = (float)mz * kp.invL[2];
-    const float m2 = fx * fx + fy * fy + fz * fz;
-    float G = 0.0f;
-    if (idx != 0) {
-      const float pi = 3.14159265358979f;
-      G = expf(-pi * pi * m2 / (kp.beta * kp.beta)) / (pi * kp.V * m2) * d.bsp[mx] *
-          d.bsp[kp.K[0] + my] * d.bsp[kp.K[0] + kp.K[1] + mz];
-    }
+    const float G = __ldg(d.ginf + idx);
     float2 *cg = d.cgrid + (size_t)r * kp.Kc + idx;
     float2 c = *cg;
     if (energy) {
+      const int mz = idx % kp.Kzc;
       const double w = (mz == 0 || (2 * mz == kp.K[2])) ? 1.0 : 2.0;
       e = w * (double)G * ((double)c.x * c.x + (double)c.y * c.y);
     }
@@ -103,6 +115,11 @@ __global__ void __launch_bounds__(256) k_solve(KParams kp, DevBufs d, int step_o
     *cg = c;
   }
   if (energy) block_atomic_add_d(0.5 * kFCoul * e, d.erec + ((size_t)(m & 1) * kp.R + r) * kNE + CPH_E_RECIP);
+}
+
+int launch_influence(Ctx &c, cudaStream_t s) {
+  k_influence<<<(c.kp.Kc + 255) / 256, 256, 0, s>>>(c.kp, c.d);
+  return 1;
 }
 
 // forces on every atom (and the fp32 phi_rec reported by cph_get_forces); the fp64 phi_rec of
