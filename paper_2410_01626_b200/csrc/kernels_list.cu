@@ -9,6 +9,8 @@
 // bit-exact against the oracle's.  Entries: sorted slot (21 bits) | LJ type (5 bits) | image
 // code (5 bits); stored in 8-entry tiles nbl[k/8][i][k%8] so the builder writes whole 32-byte
 // sectors per lane and a warp of the pair kernel reads 1 KB contiguous per 8 neighbours.
+#include <cstdlib>
+
 #include "cph_device.cuh"
 
 namespace cph {
@@ -410,6 +412,190 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
   }
 }
 
+// the canonical decision plus the canonical image code (kx+1)*9 + (ky+1)*3 + (kz+1)
+__device__ __forceinline__ bool canonical_in_code(float4 xj, float4 xi, float3 Lbox, float3 Linv, float rlist2,
+                                                  int *code) {
+  const float rx = __fsub_rn(xj.x, xi.x), ry = __fsub_rn(xj.y, xi.y), rz = __fsub_rn(xj.z, xi.z);
+  const float kx = rint_unit(__fmul_rn(rx, Linv.x)), ky = rint_unit(__fmul_rn(ry, Linv.y)),
+              kz = rint_unit(__fmul_rn(rz, Linv.z));
+  const float dx = __fsub_rn(rx, __fmul_rn(Lbox.x, kx));
+  const float dy = __fsub_rn(ry, __fmul_rn(Lbox.y, ky));
+  const float dz = __fsub_rn(rz, __fmul_rn(Lbox.z, kz));
+  *code = ((int)kx + 1) * 9 + ((int)ky + 1) * 3 + ((int)kz + 1);
+  return __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz)) < rlist2;
+}
+
+// Column builder (default).  A cell column (fixed x, y cells, all z cells) is one contiguous,
+// z-sorted slot run, so its atoms are taken 32 consecutive atoms per warp (one i atom per lane,
+// ~91 % of the lanes busy against ~56 % for one warp per cell).  For each of the 25 stencil
+// columns (raw xy offsets -2..2 with their uniform periodic images) the warp's union z window
+// [min(z_i - R_i), max(z_i + R_i)], R_i = sqrt(r_list'^2 - d_xy,i^2), selects the column's
+// cells (plus the image run when the window crosses z = 0 or L); their atoms are staged 32 at
+// a time in shared memory and each lane tests them with the image-staged fast d^2, the exact
+// canonical decision (R14, image included) inside the rounding band, and appends
+// accepted entries to its 16-entry shared-memory ring, flushed as whole 32-byte list tiles.
+constexpr int kColWarps = 8;
+
+__global__ void __launch_bounds__(32 * kColWarps) k_build_list_col(KParams kp, DevBufs d) {
+  const int r = blockIdx.y, colid = blockIdx.x;
+  const int cx = colid / kp.nc[1], cy = colid % kp.nc[1];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t base = (size_t)r * kp.Nst;
+  const float4 *xq = d.xyzq + base;
+  const int2 *meta = d.meta + base;
+  const int *start = d.cell_start + (size_t)r * (kp.ncell + 1);
+  const int nz = kp.nc[2];
+  const int cb = start[colid * nz], ce = start[colid * nz + nz];
+  const float3 Lbox = make_float3(kp.L[0], kp.L[1], kp.L[2]);
+  const float3 Linv = make_float3(kp.invL[0], kp.invL[1], kp.invL[2]);
+  const float rlist2 = kp.rlist2;
+  const float lo2 = kp.rlist2 * (1.0f - 3e-5f), hi2 = kp.rlist2 * (1.0f + 3e-5f);
+  const float csx = kp.L[0] / (float)kp.nc[0], csy = kp.L[1] / (float)kp.nc[1], csz = kp.L[2] / (float)nz;
+  const float win_r = sqrtf(kp.rlist2) * 1.0001f + kWinPad;
+  const float win_r2 = win_r * win_r;
+  __shared__ int s_colc[25], s_code[25];
+  __shared__ float s_sx[25], s_sy[25], s_xlo[25], s_ylo[25];
+  __shared__ float4 s_pos[kColWarps][32];
+  __shared__ int s_ent[kColWarps][32];
+  __shared__ uint32_t s_ring[kColWarps][16][32];
+  if (threadIdx.x < 25) {
+    const int k = c_walk[threadIdx.x * 5] / 5;            // column ring order around the centre
+    const int rx = cx - 2 + k / 5, ry = cy - 2 + k % 5;
+    const int wx = (rx + 2 * kp.nc[0]) / kp.nc[0] - 2, wy = (ry + 2 * kp.nc[1]) / kp.nc[1] - 2;
+    s_colc[threadIdx.x] = ((rx - wx * kp.nc[0]) * kp.nc[1] + (ry - wy * kp.nc[1])) * nz;
+    s_sx[threadIdx.x] = kp.L[0] * (float)wx;
+    s_sy[threadIdx.x] = kp.L[1] * (float)wy;
+    s_xlo[threadIdx.x] = (float)rx * csx - kWinPad;
+    s_ylo[threadIdx.x] = (float)ry * csy - kWinPad;
+    s_code[threadIdx.x] = (1 - wx) * 9 + (1 - wy) * 3;
+  }
+  __syncthreads();
+  float4 *sx = s_pos[w];
+  int *sj = s_ent[w];
+  uint32_t (*s_buf)[32] = s_ring[w];
+  uint32_t *nbl = d.nbl + (size_t)r * kp.cap * kp.Nst;
+  for (int i0 = cb + 32 * w; i0 < ce; i0 += 32 * kColWarps) {
+    const int i = i0 + lane;
+    const bool valid = i < ce;
+    const float4 xi = valid ? xq[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int orig = valid ? meta[i].x : 0;
+    const int eb = valid ? d.excl_ptr[orig] : 0, ee = valid ? d.excl_ptr[orig + 1] : 0;
+    uint4 *out = reinterpret_cast<uint4 *>(nbl) + 2 * (size_t)(valid ? i : 0);
+    const size_t ostride = 2 * (size_t)kp.Nst;
+    int cnt = 0, flushed = 0;
+    for (int q = 0; q < 25; ++q) {
+      const float xlo = s_xlo[q], ylo = s_ylo[q];
+      const float ddx = fmaxf(0.f, fmaxf(xlo - xi.x, xi.x - (xlo + csx + 2.f * kWinPad)));
+      const float ddy = fmaxf(0.f, fmaxf(ylo - xi.y, xi.y - (ylo + csy + 2.f * kWinPad)));
+      const float rr2 = win_r2 - ddx * ddx - ddy * ddy;
+      float zlo = INFINITY, zhi = -INFINITY;
+      if (valid && rr2 > 0.f) {
+        const float rr = sqrtf(rr2);
+        zlo = xi.z - rr;
+        zhi = xi.z + rr;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
+        zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
+      }
+      if (!(zlo <= zhi)) continue;
+      const int colc = s_colc[q];
+      const float wsx = s_sx[q], wsy = s_sy[q];
+      // runs: the home z image, the image below 0, the image above L (the union window of
+      // a warp in a short box can cross both ends; each lane's own reach R < L/2 never does)
+      for (int part = 0; part < 3; ++part) {
+        float a, b, wsz;
+        int wz;
+        if (part == 0) { a = fmaxf(zlo, 0.f); b = fminf(zhi, kp.L[2]); wsz = 0.f; wz = 0; }
+        else if (part == 1) {
+          if (!(zlo < 0.f)) continue;
+          a = zlo + kp.L[2]; b = kp.L[2]; wsz = -kp.L[2]; wz = -1;
+        } else {
+          if (!(zhi > kp.L[2])) continue;
+          a = 0.f; b = zhi - kp.L[2]; wsz = kp.L[2]; wz = 1;
+        }
+        if (!(a <= b)) continue;
+        const int c0 = max(0, min((int)floorf(a / csz), nz - 1));
+        const int c1 = max(0, min((int)floorf(b / csz), nz - 1));
+        const int j0 = start[colc + c0], j1 = start[colc + c1 + 1];
+        const int fast_code = s_code[q] + (1 - wz);
+        const float zwlo = zlo - wsz, zwhi = zhi - wsz;      // window in the staged frame's terms
+        for (int jb = j0; jb < j1; jb += 32) {
+          const int nj = min(32, j1 - jb);
+          __syncwarp();
+          float zt = 0.f;
+          if (lane < nj) {
+            const float4 p = xq[jb + lane];
+            sx[lane] = make_float4(p.x + wsx, p.y + wsy, p.z + wsz, 0.f);
+            sj[lane] = (jb + lane) | ((meta[jb + lane].y & (int)kEntryTypeMask) << kEntryTypeShift);
+            zt = p.z;
+          }
+          // the staged atoms are z-sorted: the union window is a contiguous slice
+          const int tb = __popc(__ballot_sync(0xffffffffu, lane < nj && zt < zwlo));
+          const int te = __popc(__ballot_sync(0xffffffffu, lane < nj && zt <= zwhi));
+          __syncwarp();
+          if (!valid) continue;
+          for (int t0 = tb; t0 < te; t0 += 4) {
+            float d2v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float4 xj = sx[min(t0 + u, te - 1)];
+              const float dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
+              d2v[u] = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (t0 + u >= te) continue;
+              if (d2v[u] >= hi2) continue;
+              const int je = sj[t0 + u] | (fast_code << kEntryImgShift);
+              const int j = je & (int)kEntryJMask;
+              if (d2v[u] >= lo2) {               // rounding band: exact canonical decision + image
+                int cc;
+                if (!canonical_in_code(xq[j], xi, Lbox, Linv, rlist2, &cc) || cc != fast_code) continue;
+              }
+              if (j == i) continue;
+              if (ee > eb) {                        // solute atoms only
+                const int oj = meta[j].x;
+                bool ex = false;
+                for (int e = eb; e < ee; ++e) ex |= (d.excl_idx[e] == oj);
+                if (ex) continue;
+              }
+              s_buf[cnt & 15][lane] = (uint32_t)je;
+              ++cnt;
+            }
+            if (cnt - flushed >= 8) {
+              if (flushed < kp.cap) {
+                const int h = flushed & 8;
+                out[0] = make_uint4(s_buf[h][lane], s_buf[h + 1][lane], s_buf[h + 2][lane], s_buf[h + 3][lane]);
+                out[1] = make_uint4(s_buf[h + 4][lane], s_buf[h + 5][lane], s_buf[h + 6][lane], s_buf[h + 7][lane]);
+                out += ostride;
+              }
+              flushed += 8;
+            }
+          }
+        }
+      }
+    }
+    if (valid && cnt > flushed && flushed < kp.cap) {
+      // pad the last tile with the atom's own slot (zero shift, r = 0: skipped by the pair kernel)
+      const uint32_t self = (uint32_t)i | ((uint32_t)(meta[i].y & (int)kEntryTypeMask) << kEntryTypeShift) |
+                            (13u << kEntryImgShift);
+      const int h = flushed & 8;
+      for (int k = cnt - flushed; k < 8; ++k) s_buf[h + k][lane] = self;
+      out[0] = make_uint4(s_buf[h][lane], s_buf[h + 1][lane], s_buf[h + 2][lane], s_buf[h + 3][lane]);
+      out[1] = make_uint4(s_buf[h + 4][lane], s_buf[h + 5][lane], s_buf[h + 6][lane], s_buf[h + 7][lane]);
+    }
+    if (valid) {
+      d.nnb[base + i] = cnt;
+      if (cnt > kp.cap) {
+        d.flags[FLAG_LIST_OVERFLOW] = 1;
+        atomicMax(&d.flags[FLAG_MAX_NNB], cnt);
+      }
+    }
+  }
+}
+
 // spatial sort + permutation of every per-atom array (positions wrapped); the pair list
 // itself is launch_build_list, so work that only needs the new atom order (the PME chain) can
 // start while the list is built
@@ -427,7 +613,9 @@ int launch_sort(Ctx &c, cudaStream_t s) {
 }
 
 int launch_build_list(Ctx &c, cudaStream_t s) {
-  k_build_list<<<dim3(c.kp.ncell, c.kp.R), 32, 0, s>>>(c.kp, c.d);
+  static const bool by_cell = getenv("CPH_BUILD") && getenv("CPH_BUILD")[0] == 'c';   // A/B: one warp per cell
+  if (by_cell) k_build_list<<<dim3(c.kp.ncell, c.kp.R), 32, 0, s>>>(c.kp, c.d);
+  else k_build_list_col<<<dim3(c.kp.nc[0] * c.kp.nc[1], c.kp.R), 32 * kColWarps, 0, s>>>(c.kp, c.d);
   return 1;
 }
 
