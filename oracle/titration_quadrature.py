@@ -67,3 +67,49 @@ def deprotonated_fraction(pKa, pH, T, h, kw, b=0.0, c=0.0, vmm=None, n=400001):
 
 def titration_curve(pKa, pH_levels, T, h, kw, b=0.0, c=0.0, vmm=None, n=400001):
     return np.array([deprotonated_fraction(pKa, p, T, h, kw, b, c, vmm, n) for p in pH_levels])
+
+
+# ---- His (3-state) site: 2-D in (lambda_p, lambda_t) ----------------------------------------
+def coulomb_biquadratic(rep, cp, ct):
+    """E_coul(lp, lt) - E_coul(0, 0) = sum_{a,b<=2} c[a, b] lp^a lt^b along the coordinates
+    (cp, ct) of one His group (others at rep.lam): the charges are bilinear in (lp, lt) (Eq. 2,
+    PAPER.md:621-623) and E_coul is quadratic in the charges, so degree <= 2 in each variable;
+    read off the 3 x 3 tensor grid {0, 1/2, 1}^2.  Returns (c [3, 3], check) with check the
+    deviation at (1/4, 3/4)."""
+    base = np.asarray(rep.lam, np.float64).copy()
+
+    def at(lp, lt):
+        v = base.copy()
+        v[cp], v[ct] = lp, lt
+        return coulomb_energy(rep, v)
+    nodes = np.array([0.0, 0.5, 1.0])
+    E = np.array([[at(a, b) for b in nodes] for a in nodes])
+    V = np.vander(nodes, 3, increasing=True)                  # V[i, a] = node_i^a
+    Vi = np.linalg.inv(V)
+    c = Vi @ E @ Vi.T                                        # E[i, j] = sum_ab V[i,a] c[a,b] V[j,b]
+    c[0, 0] -= E[0, 0]
+    poly = lambda lp, lt: sum(c[a, b] * lp ** a * lt ** b for a in range(3) for b in range(3))
+    check = abs(E[0, 0] + poly(0.25, 0.75) - at(0.25, 0.75))
+    return c, check
+
+
+def his_fractions(pKa3, pH, T, h, kw, c=None, vmm=None, n=1201):
+    """(x_deprot, x_delta, x_eps) of exp(-V/kT) on [LO, HI]^2 (trapezoid, n x n points):
+    V = group bias of a His site (Vdw(lp) + Vdw(lt; tautomer barrier) + VpH + Vmm, PFC depths
+    from oracle.pfc.pfc_3state) + sum c[a, b] lp^a lt^b.  Deprotonated iff
+    lp >= 0.5 (R1); delta iff lt < 0.5 (R4)."""
+    from .pfc import pfc_3state
+    d1p, d1t = pfc_3state(h, pKa3, pH, T, kw)
+    x = np.linspace(LO, HI, n)
+    LP, LT = np.meshgrid(x, x, indexing="ij")
+    c36 = np.zeros(36) if vmm is None else np.asarray(vmm, np.float64)
+    V = B.group_bias(3, c36, pKa3, pH, T, h, d1p, d1t, kw, LP, LT)[0]
+    if c is not None:
+        V = V + sum(c[a, b] * LP ** a * LT ** b for a in range(3) for b in range(3))
+    w = np.exp(-(V - V.min()) / kT(T))
+    wx = np.full(n, x[1] - x[0])
+    wx[0] = wx[-1] = 0.5 * (x[1] - x[0])
+    W = w * wx[:, None] * wx[None, :]
+    Z = W.sum()
+    dep = LP >= 0.5
+    return float(W[dep].sum() / Z), float(W[dep & (LT < 0.5)].sum() / Z), float(W[dep & (LT >= 0.5)].sum() / Z)

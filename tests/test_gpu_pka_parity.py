@@ -22,7 +22,7 @@ pytestmark = pytest.mark.gpu
 from oracle import titration_quadrature as TQ  # noqa: E402
 from oracle.analysis import fit_hh  # noqa: E402
 from oracle.engine import OracleReplica  # noqa: E402
-from synthetic.systems import make_system, replica_seeds  # noqa: E402
+from synthetic.systems import make_system, replica_seeds, small_system  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -78,3 +78,60 @@ def test_electrostatics_on_pka_matches_oracle_quadrature(cph):
     assert hi - lo < 0.05                                 # the test can resolve the bar
     assert abs(est - pka_or) <= 0.05
     assert np.all(np.abs(x_gpu - x_or) < 0.03)
+
+
+def test_electrostatics_on_his_pka_matches_oracle_quadrature(cph):
+    """The multisite case: the His group of the tiny system (HIP / HID / HIE, coordinates
+    lambda_p, lambda_t) in a frozen environment, Glu made Coulomb-free.  E_coul
+    is a polynomial of degree <= 2 in each of (lambda_p, lambda_t) (bilinear charges), read off
+    the oracle on a 3 x 3 grid; V_mm cancels 92 % of it (the remainder's negative lambda_p^2
+    curvature adds a ~2.8 kJ/mol hump, so the double-well barrier is lowered to 0.5 kJ/mol to
+    keep transitions frequent).  The oracle's deprotonated / delta /
+    eps fractions are 2-D quadratures of exp(-V/kT) with its own 3-state PFC depths; the GPU
+    titration (full step, frozen atoms) must give the same macroscopic pKa within 0.05 and the
+    tautomer populations within 0.03 per level."""
+    from paper_2410_01626_b200 import titration as T
+    s = copy.deepcopy(small_system())
+    s.mass[:] = 0.0
+    s.state_q[:7, 2] = s.state_q[:7, 0]              # Glu (group 0 + buffer): equal states
+    s.state_q[:7, 3] = s.state_q[:7, 0]
+    s.state_q[7, :] = s.state_q[7, 0]
+    s.vmm[:] = 0.0
+    h, kw, temp = 0.5, 1e6, 300.0
+    pk = tuple(float(v) for v in s.pKa[1])
+    rep = OracleReplica(s, pk[0], 1, lam0=np.zeros(3))
+    c, chk = TQ.coulomb_biquadratic(rep, 1, 2)
+    print("oracle E_coul polynomial c[a, b] (lp^a lt^b):", np.round(c, 4).tolist(), "check %.2e" % chk)
+    assert chk < 1e-6 * max(1.0, np.abs(c).max())
+    keep = 0.08
+    for a in range(3):
+        for b in range(3):
+            s.vmm[1, a * 6 + b] = -(1.0 - keep) * c[a, b]
+    levels = np.round(6.6 + np.array([-1.2, -0.8, -0.4, 0.0, 0.4, 0.8, 1.2]), 3)
+    ref = np.array([TQ.his_fractions(pk, p, temp, h, kw, c=c, vmm=s.vmm[1], n=801) for p in levels])
+    pka_or = fit_hh(levels, ref[:, 0])
+    print("oracle macro pKa %.4f (set %.2f); deprot / delta / eps" % (pka_or, pk[0]), np.round(ref, 4).tolist())
+
+    per = 128
+    pH = np.repeat(levels, per)
+    R = len(pH)
+    lam0 = np.stack([np.zeros(R), (np.arange(R) % 2).astype(float), ((np.arange(R) // 2) % 2).astype(float)], 1)
+    ctx = cph.cph_create(s, pH, replica_seeds(23, R), lambda0=lam0, barrier=h, lambda_mass=5.0,
+                         nstout=25, frame_capacity=4096)
+    ctx.cph_step(4000)
+    for r in range(R):
+        ctx.cph_get_frames(r)
+    ctx.cph_step(60000)
+    fr = np.stack([ctx.cph_get_frames(r)[0] for r in range(R)])          # [R, F, C]
+    assert fr.shape[1] == 2400 and np.all(np.isfinite(fr))
+    dep = fr[:, :, 1] >= 0.5
+    xr = dep.mean(1).reshape(len(levels), per)
+    xd = (dep & (fr[:, :, 2] < 0.5)).mean(1).reshape(len(levels), per).mean(1)
+    xe = (dep & (fr[:, :, 2] >= 0.5)).mean(1).reshape(len(levels), per).mean(1)
+    est, lo, hi = T.bootstrap(levels, xr, B=1000)
+    print("GPU macro pKa %.4f  95%% CI [%.4f, %.4f]; |dpKa| = %.4f" % (est, lo, hi, abs(est - pka_or)))
+    print("GPU deprot", np.round(xr.mean(1), 4).tolist(), "delta", np.round(xd, 4).tolist(), "eps", np.round(xe, 4).tolist())
+    assert abs(pka_or - pk[0]) > 0.2                         # the Coulomb remainder moves the pKa
+    assert hi - lo < 0.05
+    assert abs(est - pka_or) <= 0.05
+    assert np.all(np.abs(xd - ref[:, 1]) < 0.03) and np.all(np.abs(xe - ref[:, 2]) < 0.03)

@@ -72,3 +72,30 @@ def test_quadrature_matches_oracle_lambda_dynamics():
     fr = fr[150:]
     x = np.array([analysis.deprotonated_fraction(fr[:, k * M:(k + 1) * M]) for k in range(2)])
     assert np.all(np.abs(x - ref) < 0.02), (x, ref)
+
+
+def test_his_quadrature_without_coulomb_is_the_micro_pka_closed_form():
+    """2-D quadrature, no Coulomb term: the 3-state PFC makes the populations 1 : 10^(pH - pKa_d) :
+    10^(pH - pKa_e) (Table 2 micro pKa)."""
+    pk = (6.38, 6.53, 6.92)
+    for pH in (6.0, 6.9):
+        dep, d, e = TQ.his_fractions(pk, pH, 300.0, 2.0, 1e6, n=801)
+        wd, we = 10 ** (pH - pk[1]), 10 ** (pH - pk[2])
+        assert abs(d - wd / (1 + wd + we)) < 1e-3 and abs(e - we / (1 + wd + we)) < 1e-3
+        assert abs(dep - d - e) < 1e-12
+
+
+def test_his_biquadratic_matches_engine_dvdl():
+    """The 3 x 3 read-off of E_coul(lp, lt) against the engine's analytic dV_coul/dlp, dV_coul/dlt
+    at an interior point (a wrong Vandermonde inverse or a missing cross term fails)."""
+    from synthetic.systems import small_system
+    s = copy.deepcopy(small_system())
+    s.mass[:] = 0.0
+    rep = OracleReplica(s, 6.4, 1, lam0=np.array([0.3, 0.0, 0.0]))
+    c, chk = TQ.coulomb_biquadratic(rep, 1, 2)
+    assert chk < 1e-8 * max(1.0, np.abs(c).max())
+    lp, lt = 0.35, 0.6
+    g = rep.evaluate(rep.x, np.array([0.3, lp, lt]))["dvdl_coul"]
+    dp = sum(a * c[a, b] * lp ** (a - 1) * lt ** b for a in range(1, 3) for b in range(3))
+    dt = sum(b * c[a, b] * lp ** a * lt ** (b - 1) for a in range(3) for b in range(1, 3))
+    assert abs(g[1] - dp) < 1e-6 * max(1.0, abs(dp)) and abs(g[2] - dt) < 1e-6 * max(1.0, abs(dt))
