@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define CPH_ABI_VERSION 2
+#define CPH_ABI_VERSION 3
 
 typedef struct cph_ctx cph_ctx;
 
@@ -184,6 +184,12 @@ typedef struct {
    * and exact Ewald reciprocal terms); its lambda derivative is part of the Coulomb
    * dV/dlambda and its forces of the atom forces.  Groups of at most 32 atoms. */
   int32_t hamiltonian;
+  /* 0: PME spread with fp32 atomics (default; runs agree to rounding); 1: the spread
+   * accumulates in 64-bit fixed point (2^-40 e resolution, integer atomics commute), so the
+   * whole Langevin step is bitwise reproducible run to run (SURVEY §5 optional fixed-point
+   * accumulation); 64 integer atomics per atom instead of 16-32 float4 ones plus one grid
+   * conversion pass. */
+  int32_t deterministic;
 } cph_params;
 
 /* DBO event kinds (cph_dbo_event.kind) */

@@ -18,7 +18,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CPH_LIB", os.path.join(_HERE, "libcph.so"))   # CPH_LIB: A/B builds
 
-CPH_ABI_VERSION = 2
+CPH_ABI_VERSION = 3
 STATUS = {0: "CPH_OK", 1: "CPH_E_INVALID", 2: "CPH_E_CUDA", 3: "CPH_E_DIVERGED", 4: "CPH_E_STATE",
           5: "CPH_E_OOM", 6: "CPH_E_UNSUPPORTED"}
 ENERGY_TERMS = ("LJ", "real", "excl", "self", "recip", "net", "hi", "bias", "KE_atoms", "KE_lambda", "total")
@@ -58,7 +58,7 @@ class cph_params(C.Structure):
                 ("dbo_barrier_min", C.c_double), ("dbo_barrier_max", C.c_double),
                 ("thermostat", C.c_int32), ("tau_atom", C.c_double), ("tau_lambda", C.c_double),
                 ("n_ph_levels", C.c_int32), ("ph_levels", _f64p), ("remd_first", C.c_int32),
-                ("remd_total", C.c_int32), ("hamiltonian", C.c_int32)]
+                ("remd_total", C.c_int32), ("hamiltonian", C.c_int32), ("deterministic", C.c_int32)]
 
 
 class cph_dbo_event(C.Structure):
@@ -172,7 +172,7 @@ _FLOAT_PARAMS = ("dt", "temperature", "gamma_atom", "gamma_lambda", "lambda_mass
                  "dbo_well_gain", "dbo_well_cap", "dbo_trans_lo", "dbo_trans_hi", "dbo_target", "dbo_target_tol",
                  "dbo_barrier_step", "dbo_barrier_min", "dbo_barrier_max")
 _INT_PARAMS = ("pme_order", "nstlist", "nstout", "nstenergy", "frame_capacity", "dbo_well", "dbo_barrier",
-               "dbo_well_steps", "dbo_barrier_steps", "dbo_censor_steps", "hamiltonian")
+               "dbo_well_steps", "dbo_barrier_steps", "dbo_censor_steps", "hamiltonian", "deterministic")
 KNOWN_PARAMS = frozenset(_FLOAT_PARAMS + _INT_PARAMS + ("thermostat", "pme_grid"))
 
 

@@ -46,6 +46,7 @@ struct KParams {
   int nc[3], ncell;            // cells per dimension, total
   int ns[3], so[3];            // stencil sizes and first offsets per dimension
   int nb_packed;               // pair kernel: FFMA2 path for non-lambda warps (A/B: CPH_NB_PACKED=0)
+  int det;                     // deterministic (fixed-point) PME spread
   // list
   int cap;                     // neighbour capacity per atom
   // PME
@@ -96,6 +97,7 @@ struct DevBufs {
   float2 *cgrid = nullptr;                          // [R*Kc]
   float *bsp = nullptr;                             // [Kx + Ky + Kz] |b|^2 moduli
   float *ginf = nullptr;                            // [Kc] influence function G(m) (replica independent)
+  unsigned long long *grid_fx = nullptr;            // [R*K3] fixed-point spread accumulator (deterministic mode)
   int *g_kind = nullptr, *g_ptr = nullptr, *g_atoms = nullptr, *g_cptr = nullptr;
   double *g_q = nullptr;                            // [nlam*4]
   double *vmm = nullptr;                            // [G*36]

@@ -459,6 +459,7 @@ void cph_default_params(cph_params *p) {
   p->remd_first = 0;
   p->remd_total = 0;
   p->hamiltonian = 0;
+  p->deterministic = 0;
 }
 
 const char *cph_last_error(const cph_ctx *ctx) { return ctx ? ctx->c.err.c_str() : g_create_err.c_str(); }
@@ -506,6 +507,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   if (prm->mode != 0 && prm->mode != 1) return bad("mode must be 0 or 1");
   if (prm->thermostat != 0 && prm->thermostat != 1) return bad("thermostat must be 0 (Langevin) or 1 (Bussi)");
   if (prm->hamiltonian != 0 && prm->hamiltonian != 1) return bad("hamiltonian must be 0 or 1");
+  if (prm->deterministic != 0 && prm->deterministic != 1) return bad("deterministic must be 0 or 1");
   if (prm->thermostat == 1 && !(prm->tau_atom > 0.0 && prm->tau_lambda > 0.0))
     return bad("Bussi coupling times must be > 0");
   std::vector<int> labels0;
@@ -652,6 +654,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     kp.ncell *= nc;
   }
   kp.nb_packed = getenv("CPH_NB_PACKED") ? atoi(getenv("CPH_NB_PACKED")) : 1;
+  kp.det = prm->deterministic;
   {
     const double expect = (double)N / V * 4.0 / 3.0 * kPi * std::pow(prm->rlist, 3);
     kp.cap = (int)std::ceil(1.6 * expect + 64.0);
@@ -788,6 +791,10 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   d.cgrid = dalloc<float2>(c, (size_t)R * kp.Kc);
   d.bsp = dalloc<float>(c, kp.K[0] + kp.K[1] + kp.K[2]);
   d.ginf = dalloc<float>(c, kp.Kc);
+  if (kp.det) {
+    d.grid_fx = dalloc<unsigned long long>(c, (size_t)R * kp.K3);
+    if (!d.grid_fx) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
+  }
   d.g_kind = dalloc<int>(c, G); d.g_ptr = dalloc<int>(c, G + 1);
   d.g_atoms = dalloc<int>(c, nlam); d.g_cptr = dalloc<int>(c, G + 1);
   d.g_q = dalloc<double>(c, 4 * (size_t)nlam);
@@ -1779,7 +1786,7 @@ cph_status cph_profile_steps(cph_ctx *ctx, int64_t n_steps, double *ms, int64_t 
     { int q = launch_integrate(c, s, 1); k += q; cnt[CPH_K_INTEGRATE] += q; mark(CPH_K_INTEGRATE); }
     if (rebuild) { int q = launch_rebuild(c, s); k += q; cnt[CPH_K_PAIRLIST] += q; mark(CPH_K_PAIRLIST); }
     { int q = launch_nonbonded(c, s, 1); k += q; cnt[CPH_K_NONBONDED] += q; mark(CPH_K_NONBONDED); }
-    k += launch_spread(c, s); cnt[CPH_K_SPREAD] += 1; mark(CPH_K_SPREAD);
+    { int q = launch_spread(c, s); k += q; cnt[CPH_K_SPREAD] += q; mark(CPH_K_SPREAD); }
     cufftExecR2C(c.plan_r2c, c.d.grid, (cufftComplex *)c.d.cgrid); mark(CPH_K_FFT_R2C);
     k += launch_solve(c, s, 1); cnt[CPH_K_SOLVE] += 1; mark(CPH_K_SOLVE);
     cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid); mark(CPH_K_FFT_C2R);

@@ -4,6 +4,8 @@
 // k = floor(u) - j, j = 0..3 (mod K).  With w = u - floor(u):
 //   theta_0 = w^3/6, theta_1 = (-3w^3+3w^2+3w+1)/6, theta_2 = (3w^3-6w^2+4)/6, theta_3 = (1-w)^3/6.
 // The FFTs are cuFFT plans (reported as their own line item).
+#include <algorithm>
+
 #include "cph_device.cuh"
 
 namespace cph {
@@ -67,6 +69,50 @@ __global__ void SPREAD_ATTR k_spread(KParams kp, DevBufs d) {
         for (int c = 0; c < 4; ++c) atomicAdd(row + iz[c], qab * tz[c]);
       }
     }
+  }
+}
+
+// Deterministic mode (cph_params.deterministic): the same per-point contributions, converted
+// to 64-bit fixed point (2^-40 e) and added with integer atomics, which commute, so the grid is
+// bitwise independent of the order in which atoms arrive; k_fx_to_float converts it for the
+// FFT and clears the accumulator for the next spread.
+constexpr float kFxScale = 1099511627776.0f;          // 2^40
+constexpr double kFxInv = 1.0 / 1099511627776.0;
+
+__global__ void __launch_bounds__(128) k_spread_fx(KParams kp, DevBufs d) {
+  const int r = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= kp.N) return;
+  const float4 p = d.xyzq[(size_t)r * kp.Nst + i];
+  if (p.w == 0.0f) return;
+  int kx, ky, kz;
+  float tx[4], ty[4], tz[4], dd[4];
+  bspline4(p.x, kp.invL[0], kp.K[0], kx, tx, dd);
+  bspline4(p.y, kp.invL[1], kp.K[1], ky, ty, dd);
+  bspline4(p.z, kp.invL[2], kp.K[2], kz, tz, dd);
+  unsigned long long *g = d.grid_fx + (size_t)r * kp.K3;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int ix = (kx - a + kp.K[0]) % kp.K[0];
+    const float qa = p.w * tx[a];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int iy = (ky - b + kp.K[1]) % kp.K[1];
+      const float qab = qa * ty[b];
+      unsigned long long *row = g + ((size_t)ix * kp.K[1] + iy) * kp.K[2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const long long v = __float2ll_rn(qab * tz[c] * kFxScale);
+        atomicAdd(row + (kz - c + kp.K[2]) % kp.K[2], (unsigned long long)v);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_fx_to_float(KParams kp, DevBufs d) {
+  const size_t n = (size_t)kp.R * kp.K3;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
+    d.grid[t] = (float)((double)(long long)d.grid_fx[t] * kFxInv);
+    d.grid_fx[t] = 0ull;
   }
 }
 
@@ -165,6 +211,12 @@ __global__ void __launch_bounds__(128) k_gather(KParams kp, DevBufs d) {
 }
 
 int launch_spread(Ctx &c, cudaStream_t s) {
+  if (c.kp.det) {
+    k_spread_fx<<<dim3((c.kp.N + 127) / 128, c.kp.R), 128, 0, s>>>(c.kp, c.d);
+    const size_t n = (size_t)c.kp.R * c.kp.K3;
+    k_fx_to_float<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(c.kp, c.d);
+    return 2;
+  }
   cudaMemsetAsync(c.d.grid, 0, sizeof(float) * (size_t)c.kp.R * c.kp.K3, s);
   dim3 grid((c.kp.N + CPH_SPREAD_TPB - 1) / CPH_SPREAD_TPB, c.kp.R);
   k_spread<<<grid, CPH_SPREAD_TPB, 0, s>>>(c.kp, c.d);

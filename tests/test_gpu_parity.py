@@ -497,3 +497,24 @@ def test_c1_200_step_trajectory_diagnostic(cph):
         dx, dl = float(np.abs(d).max()), float(np.abs(lam - ref.lam).max())
         print(f"step {target}: max|dx| {dx:.3e} nm, max|dlambda| {dl:.3e}")
         assert dx < tol_x and dl < tol_l
+
+
+def test_deterministic_mode_bitwise_reproducible_and_parity(cph):
+    """deterministic = 1 (fixed-point PME spread): two runs from the same inputs agree bit for
+    bit after 37 steps (rebuilds included) - the default fp32-atomic spread agrees only to
+    rounding - and the snapshot still matches the oracle."""
+    s = make_system(1)
+    runs = []
+    for _ in range(2):
+        ctx, lam0, pH, seeds, vel = _ctx(cph, s, 2, seed=5, deterministic=1)
+        if not runs:
+            for r in range(2):
+                ref = OracleReplica(s, pH[r], int(seeds[r]), lam0=lam0[r], vel0=vel[r])
+                err = compare_snapshot(ctx, r, ref, lam_atoms=s.group_atoms)
+                assert err["force"] <= RTOL and err["force_atom"] <= RTOL and err["dvdl_coul"] <= RTOL
+                assert err["E_total"] <= ETOL
+        ctx.cph_step(37)
+        runs.append([(ctx.cph_get_positions(r), ctx.cph_get_lambdas(r)) for r in range(2)])
+    for (xa, la), (xb, lb) in zip(runs[0], runs[1]):
+        assert np.array_equal(xa[0], xb[0]) and np.array_equal(xa[1], xb[1])
+        assert np.array_equal(la[0], lb[0]) and np.array_equal(la[1], lb[1])
