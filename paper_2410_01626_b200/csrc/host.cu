@@ -289,9 +289,30 @@ int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
   // anything that reads f_rec)
   if (two_streams) cudaEventRecord(c.ev_join, c.stream_pme);
   else k += launch_gather(c, s);
-  if (two_streams && c.prio) {
+  static const bool lam_low = getenv("CPH_LAMBDA_LOWPRIO") != nullptr;   // A/B: round-1 placement
+  if (two_streams && c.prio && !lam_low) {
     // the pair kernel on a high-priority stream: the PME chain (low priority) fills the SMs
-    // the pair kernel leaves free instead of displacing its CTAs
+    // the pair kernel leaves free instead of displacing its CTAs.  The lambda kernel (one CTA
+    // per replica, the end of the step's critical path) follows on the same high-priority
+    // stream once the back transform is done, so its CTAs are not queued behind the
+    // all-atom gather's thousands of CTAs on the PME stream.
+    cudaEventRecord(c.ev_fork2, s);
+    cudaStreamWaitEvent(c.stream_nb, c.ev_fork2, 0);
+    k += launch_nonbonded(c, c.stream_nb, 1);
+    tl_mark(c, c.stream_nb, 8);
+    k += launch_gather(c, c.stream_pme);
+    tl_mark(c, c.stream_pme, 9);
+    cudaEventRecord(c.ev_gather, c.stream_pme);
+    cudaStreamWaitEvent(c.stream_nb, c.ev_join, 0);
+    k += launch_hi_finish(c, c.stream_nb, 1);
+    k += launch_lambda_reduce(c, c.stream_nb, 1);
+    tl_mark(c, c.stream_nb, 10);
+    cudaEventRecord(c.ev_join2, c.stream_nb);
+    cudaStreamWaitEvent(s, c.ev_join2, 0);
+    cudaStreamWaitEvent(s, c.ev_gather, 0);
+    return k;
+  }
+  if (two_streams && c.prio) {
     cudaEventRecord(c.ev_fork2, s);
     cudaStreamWaitEvent(c.stream_nb, c.ev_fork2, 0);
     k += launch_nonbonded(c, c.stream_nb, 1);
