@@ -325,8 +325,11 @@ def main():
     ctx.cph_sync()
     alg = algorithmic(s, R)
     hbm, hbm_kind = peaks()
-    # cuFFT executions are not counted by the library (one R2C and one C2R plan execution per step)
-    execs = {k: (prof_n[k] if prof_n.get(k) else (args.profile_steps if k.startswith("fft") else 0)) for k in prof_ms}
+    # cuFFT executions are not counted by the library (one R2C and one C2R plan execution per
+    # step and replica sub-batch; the sub-batches' launches of a class run side by side)
+    S = ctx.sub_batches
+    execs = {k: (prof_n[k] if prof_n.get(k) else (S * args.profile_steps if k.startswith("fft") else 0))
+             for k in prof_ms}
     per = {k: prof_ms[k] / execs[k] for k in prof_ms if execs[k]}
     total_prof = sum(prof_ms.values())
     kernels = {}
@@ -335,7 +338,9 @@ def main():
             "fft_r2c": ("hbm", alg["fft_bytes_each"], "GB/s"), "fft_c2r": ("hbm", alg["fft_bytes_each"], "GB/s"),
             "integrate": ("hbm", alg["integrate_bytes"], "GB/s")}
     for k, t_ms in per.items():
-        ent = {"ms_per_launch": t_ms, "launches_per_step": execs[k] / args.profile_steps,
+        # ms_per_launch: one launch over the whole batch (the S sub-batch launches side by side)
+        ent = {"ms_per_launch": t_ms * S, "ms_per_step": prof_ms[k] / args.profile_steps,
+               "launches_per_step": execs[k] / args.profile_steps,
                "share_of_step": prof_ms[k] / total_prof if total_prof else None}
         if k in work and t_ms > 0:
             bound, amount, unit = work[k]
@@ -426,6 +431,7 @@ def main():
         "config": {"workload": s.name, "atoms": s.n_atoms, "replicas_per_gpu": R, "pme_grid": list(s.pme_grid),
                    "lambda_groups": s.n_groups, "lambda_coords": s.n_coords, "pH_points": len(s.pH_grid),
                    "parallelism": f"replicas x{world} (one process per GPU)",
+                   "sub_batches": S,
                    "l2": "inputs exceed L2 (no flush): per-step pair-list + grid stream > 126 MB"},
         "ns_per_day_per_system": ns_day_system, "lambda_steps_per_s_per_system": steps_per_s,
         "lambda_coord_updates_per_s": steps_per_s * s.n_coords * R * world,

@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define CPH_ABI_VERSION 3
+#define CPH_ABI_VERSION 4
 
 typedef struct cph_ctx cph_ctx;
 
@@ -190,6 +190,17 @@ typedef struct {
    * accumulation); 64 integer atomics per atom instead of 16-32 float4 ones plus one grid
    * conversion pass. */
   int32_t deterministic;
+  /* Replica sub-batches stepped concurrently (0 = automatic, the default; 1 = one batch).
+   * The R replicas are split into S consecutive, near-equal batches, each with its own
+   * device buffers, CUDA graph and stream; cph_step interleaves them in chunks of 32 nstlist
+   * blocks, so one batch's PME chain (FFTs, solve, gather: few CTAs) runs under another's
+   * pair kernel instead of leaving SMs idle at the end of every step.  Every random number
+   * is keyed on (replica seed, step, atom) and every kernel works per replica, so results
+   * are those of one batch up to rounding (identical trajectories in tests/test_gpu_subbatch.py).
+   * Automatic: S = min(R, 4) when R * n_atoms >= 24000, else 1.  Every call
+   * stays ordered on cph_get_stream(); per-replica getters route to the batch holding the
+   * replica. */
+  int32_t sub_batches;
 } cph_params;
 
 /* DBO event kinds (cph_dbo_event.kind) */
@@ -225,6 +236,8 @@ void cph_destroy(cph_ctx *ctx);
 int32_t cph_n_coords(const cph_ctx *ctx);
 int32_t cph_n_atoms(const cph_ctx *ctx);
 int32_t cph_n_replicas(const cph_ctx *ctx);
+/* Number of replica sub-batches S the context steps concurrently (cph_params.sub_batches). */
+int32_t cph_n_sub_batches(const cph_ctx *ctx);
 
 /* The CUDA stream every call of this context enqueues on (the cph_params.cuda_stream the
  * caller passed, or the context's own non-blocking stream when that was NULL). */

@@ -18,7 +18,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CPH_LIB", os.path.join(_HERE, "libcph.so"))   # CPH_LIB: A/B builds
 
-CPH_ABI_VERSION = 3
+CPH_ABI_VERSION = 4
 STATUS = {0: "CPH_OK", 1: "CPH_E_INVALID", 2: "CPH_E_CUDA", 3: "CPH_E_DIVERGED", 4: "CPH_E_STATE",
           5: "CPH_E_OOM", 6: "CPH_E_UNSUPPORTED"}
 ENERGY_TERMS = ("LJ", "real", "excl", "self", "recip", "net", "hi", "bias", "KE_atoms", "KE_lambda", "total")
@@ -58,7 +58,8 @@ class cph_params(C.Structure):
                 ("dbo_barrier_min", C.c_double), ("dbo_barrier_max", C.c_double),
                 ("thermostat", C.c_int32), ("tau_atom", C.c_double), ("tau_lambda", C.c_double),
                 ("n_ph_levels", C.c_int32), ("ph_levels", _f64p), ("remd_first", C.c_int32),
-                ("remd_total", C.c_int32), ("hamiltonian", C.c_int32), ("deterministic", C.c_int32)]
+                ("remd_total", C.c_int32), ("hamiltonian", C.c_int32), ("deterministic", C.c_int32),
+                ("sub_batches", C.c_int32)]
 
 
 class cph_dbo_event(C.Structure):
@@ -77,6 +78,7 @@ EXPORTS = {
     "cph_n_coords": (C.c_int32, [C.c_void_p]),
     "cph_n_atoms": (C.c_int32, [C.c_void_p]),
     "cph_n_replicas": (C.c_int32, [C.c_void_p]),
+    "cph_n_sub_batches": (C.c_int32, [C.c_void_p]),
     "cph_set_pH": (C.c_int, [C.c_void_p, C.c_int32, C.c_double]),
     "cph_step": (C.c_int, [C.c_void_p, C.c_int64]),
     "cph_sync": (C.c_int, [C.c_void_p]),
@@ -172,7 +174,8 @@ _FLOAT_PARAMS = ("dt", "temperature", "gamma_atom", "gamma_lambda", "lambda_mass
                  "dbo_well_gain", "dbo_well_cap", "dbo_trans_lo", "dbo_trans_hi", "dbo_target", "dbo_target_tol",
                  "dbo_barrier_step", "dbo_barrier_min", "dbo_barrier_max")
 _INT_PARAMS = ("pme_order", "nstlist", "nstout", "nstenergy", "frame_capacity", "dbo_well", "dbo_barrier",
-               "dbo_well_steps", "dbo_barrier_steps", "dbo_censor_steps", "hamiltonian", "deterministic")
+               "dbo_well_steps", "dbo_barrier_steps", "dbo_censor_steps", "hamiltonian", "deterministic",
+               "sub_batches")
 KNOWN_PARAMS = frozenset(_FLOAT_PARAMS + _INT_PARAMS + ("thermostat", "pme_grid"))
 
 
@@ -285,6 +288,7 @@ class Context:
         self._cbs = callbacks            # keep allocator callbacks alive
         self.C = lib().cph_n_coords(handle)
         self.N = lib().cph_n_atoms(handle)
+        self.sub_batches = lib().cph_n_sub_batches(handle)
 
     def close(self):
         if self.h:

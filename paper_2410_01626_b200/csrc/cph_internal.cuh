@@ -185,6 +185,7 @@ struct Ctx {
   std::vector<int> h_c_group, h_c_lp;               // [C]
   std::vector<long long> h_cens;                    // [R*G*2]
   std::vector<cph_dbo_event> events;                // undrained DBO log
+  int *h_bad = nullptr;                             // pinned: FLAG_BAD_STATE read back by set_state
   std::vector<double> h_levels;                     // [P] pH ladder
   std::vector<double> h_lvl_d1, h_lvl_dG;           // [P*C], [P*G*3]
   DboConfig dbo;

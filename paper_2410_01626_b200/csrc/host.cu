@@ -26,7 +26,7 @@ struct NvtxRange {
 };
 #define CPH_NVTX(name) NvtxRange nvtx_range_(name)
 
-struct cph_ctx {
+struct SubCtx {
   Ctx c;
 };
 
@@ -433,7 +433,6 @@ cph_status check_replica(Ctx &c, int r) {
 
 }  // namespace
 
-extern "C" {
 
 void cph_default_params(cph_params *p) {
   std::memset(p, 0, sizeof(*p));
@@ -481,23 +480,23 @@ void cph_default_params(cph_params *p) {
   p->remd_total = 0;
   p->hamiltonian = 0;
   p->deterministic = 0;
+  p->sub_batches = 0;
 }
 
-const char *cph_last_error(const cph_ctx *ctx) { return ctx ? ctx->c.err.c_str() : g_create_err.c_str(); }
 
-static cph_status fail_create(cph_ctx *ctx, cph_status st) {
+static cph_status fail_create(SubCtx *ctx, cph_status st) {
   g_create_err = ctx->c.err;
   free_all(ctx->c);
   delete ctx;
   return st;
 }
 
-cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **out) {
+static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCtx **out) {
   CPH_NVTX("cph_create");
   if (!out) { g_create_err = "out is NULL"; return CPH_E_INVALID; }
   *out = nullptr;
   if (!sys || !prm) { g_create_err = "system/params is NULL"; return CPH_E_INVALID; }
-  cph_ctx *ctx = new cph_ctx;
+  SubCtx *ctx = new SubCtx;
   Ctx &c = ctx->c;
   auto bad = [&](const char *m) { c.err = m; return fail_create(ctx, CPH_E_INVALID); };
   if (prm->abi_version != CPH_ABI_VERSION) return bad("abi_version mismatch");
@@ -1008,7 +1007,7 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
   return CPH_OK;
 }
 
-void cph_destroy(cph_ctx *ctx) {
+static void sub_destroy(SubCtx *ctx) {
   if (!ctx) return;
   Ctx &c = ctx->c;
   cudaSetDevice(c.device);
@@ -1018,6 +1017,7 @@ void cph_destroy(cph_ctx *ctx) {
   if (c.plan_r2c) cufftDestroy(c.plan_r2c);
   if (c.plan_c2r) cufftDestroy(c.plan_c2r);
   free_all(c);
+  if (c.h_bad) cudaFreeHost(c.h_bad);
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
   if (c.ev_join) cudaEventDestroy(c.ev_join);
   if (c.ev_gather) cudaEventDestroy(c.ev_gather);
@@ -1029,14 +1029,12 @@ void cph_destroy(cph_ctx *ctx) {
   delete ctx;
 }
 
-void *cph_get_stream(const cph_ctx *ctx) { return ctx ? (void *)ctx->c.stream : nullptr; }
-int32_t cph_n_coords(const cph_ctx *ctx) { return ctx ? ctx->c.kp.C : -1; }
-int32_t cph_n_atoms(const cph_ctx *ctx) { return ctx ? ctx->c.kp.N : -1; }
-int32_t cph_n_replicas(const cph_ctx *ctx) { return ctx ? ctx->c.kp.R : -1; }
-int64_t cph_current_step(const cph_ctx *ctx) { return ctx ? ctx->c.host_step : -1; }
-int64_t cph_launch_count(const cph_ctx *ctx) { return ctx ? ctx->c.launches : -1; }
+static int32_t sub_n_coords(const SubCtx *ctx) { return ctx ? ctx->c.kp.C : -1; }
+static int32_t sub_n_atoms(const SubCtx *ctx) { return ctx ? ctx->c.kp.N : -1; }
+static int64_t sub_current_step(const SubCtx *ctx) { return ctx ? ctx->c.host_step : -1; }
+static int64_t sub_launch_count(const SubCtx *ctx) { return ctx ? ctx->c.launches : -1; }
 
-cph_status cph_set_pH(cph_ctx *ctx, int32_t replica, double pH) {
+static cph_status sub_set_pH(SubCtx *ctx, int32_t replica, double pH) {
   CPH_NVTX("cph_set_pH");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
@@ -1181,7 +1179,7 @@ static long long next_dbo_boundary(const Ctx &c) {
   return nb;
 }
 
-cph_status cph_step(cph_ctx *ctx, int64_t n_steps) {
+static cph_status sub_step(SubCtx *ctx, int64_t n_steps) {
   CPH_NVTX("cph_step");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
@@ -1198,44 +1196,44 @@ cph_status cph_step(cph_ctx *ctx, int64_t n_steps) {
   return CPH_OK;
 }
 
-cph_status cph_sync(cph_ctx *ctx) {
+static cph_status sub_sync(SubCtx *ctx) {
   CPH_NVTX("cph_sync");
   if (!ctx) return CPH_E_INVALID;
   cudaSetDevice(ctx->c.device);
   return check_flags(ctx->c);
 }
 
-cph_status cph_get_lambdas(cph_ctx *ctx, int32_t r, double *lam, double *vel) {
+static cph_status sub_get_lambdas(SubCtx *ctx, int32_t r, double *lam, double *vel) {
   CPH_NVTX("cph_get_lambdas");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   const size_t C = c.kp.C;
   if (lam && C) CK(cudaMemcpy(lam, c.d.lam + r * C, sizeof(double) * C, cudaMemcpyDeviceToHost));
   if (vel && C) CK(cudaMemcpy(vel, c.d.lamv + r * C, sizeof(double) * C, cudaMemcpyDeviceToHost));
   return CPH_OK;
 }
 
-cph_status cph_get_dvdl(cph_ctx *ctx, int32_t r, double *coul, double *bias) {
+static cph_status sub_get_dvdl(SubCtx *ctx, int32_t r, double *coul, double *bias) {
   CPH_NVTX("cph_get_dvdl");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   const size_t C = c.kp.C;
   if (coul && C) CK(cudaMemcpy(coul, c.d.dvdl_coul + r * C, sizeof(double) * C, cudaMemcpyDeviceToHost));
   if (bias && C) CK(cudaMemcpy(bias, c.d.dvdl_bias + r * C, sizeof(double) * C, cudaMemcpyDeviceToHost));
   return CPH_OK;
 }
 
-cph_status cph_get_bias_params(cph_ctx *ctx, int32_t r, double *d1) {
+static cph_status sub_get_bias_params(SubCtx *ctx, int32_t r, double *d1) {
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
   if (st) return st;
   if (d1 && c.kp.P) {          // labels may have moved on the device
-    if ((st = cph_sync(ctx))) return st;
+    if ((st = sub_sync(ctx))) return st;
     if (c.kp.C) CK(cudaMemcpy(d1, c.d.d1 + (size_t)r * c.kp.C, sizeof(double) * c.kp.C, cudaMemcpyDeviceToHost));
     return CPH_OK;
   }
@@ -1243,12 +1241,12 @@ cph_status cph_get_bias_params(cph_ctx *ctx, int32_t r, double *d1) {
   return CPH_OK;
 }
 
-cph_status cph_get_energies(cph_ctx *ctx, int32_t r, double *e) {
+static cph_status sub_get_energies(SubCtx *ctx, int32_t r, double *e) {
   CPH_NVTX("cph_get_energies");
   if (!ctx || !e) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   const size_t off = ((size_t)(c.host_step & 1) * c.kp.R + r) * kNE;
   CK(cudaMemcpy(e, c.d.erec + off, sizeof(double) * kNE, cudaMemcpyDeviceToHost));
   double tot = 0.0;
@@ -1257,13 +1255,13 @@ cph_status cph_get_energies(cph_ctx *ctx, int32_t r, double *e) {
   return CPH_OK;
 }
 
-cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t r, float *buf, uint8_t *censored, int64_t *steps, int32_t *labels,
+static cph_status sub_get_frames_ex(SubCtx *ctx, int32_t r, float *buf, uint8_t *censored, int64_t *steps, int32_t *labels,
                              int64_t cap, int64_t *n_frames, int64_t *n_dropped) {
   CPH_NVTX("cph_get_frames_ex");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   if (cap < 0) { c.err = "cap < 0"; return CPH_E_INVALID; }
   const KParams &kp = c.kp;
   long long total = 0;
@@ -1298,8 +1296,8 @@ cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t r, float *buf, uint8_t *censo
   return CPH_OK;
 }
 
-cph_status cph_get_frames(cph_ctx *ctx, int32_t r, float *buf, int64_t cap, int64_t *n_frames, int64_t *n_dropped) {
-  return cph_get_frames_ex(ctx, r, buf, nullptr, nullptr, nullptr, cap, n_frames, n_dropped);
+static cph_status sub_get_frames(SubCtx *ctx, int32_t r, float *buf, int64_t cap, int64_t *n_frames, int64_t *n_dropped) {
+  return sub_get_frames_ex(ctx, r, buf, nullptr, nullptr, nullptr, cap, n_frames, n_dropped);
 }
 
 static cph_status need_remd(Ctx &c) {
@@ -1307,7 +1305,7 @@ static cph_status need_remd(Ctx &c) {
   return CPH_OK;
 }
 
-cph_status cph_exchange_energies(cph_ctx *ctx, double *rows) {
+static cph_status sub_exchange_energies(SubCtx *ctx, double *rows) {
   CPH_NVTX("cph_exchange_energies");
   if (!ctx || !rows) return CPH_E_INVALID;
   Ctx &c = ctx->c;
@@ -1318,7 +1316,7 @@ cph_status cph_exchange_energies(cph_ctx *ctx, double *rows) {
   return CPH_OK;
 }
 
-cph_status cph_exchange_apply(cph_ctx *ctx, const double *rows_all, uint64_t seed, int64_t attempt) {
+static cph_status sub_exchange_apply(SubCtx *ctx, const double *rows_all, uint64_t seed, int64_t attempt) {
   CPH_NVTX("cph_exchange_apply");
   if (!ctx || !rows_all || attempt < 0) return CPH_E_INVALID;
   Ctx &c = ctx->c;
@@ -1330,25 +1328,25 @@ cph_status cph_exchange_apply(cph_ctx *ctx, const double *rows_all, uint64_t see
   return CPH_OK;
 }
 
-cph_status cph_exchange(cph_ctx *ctx, uint64_t seed, int64_t attempt) {
+static cph_status sub_exchange(SubCtx *ctx, uint64_t seed, int64_t attempt) {
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   if (cph_status st = need_remd(c)) return st;
   if (c.kp.remd_total != c.kp.R) { c.err = "cph_exchange needs every replica in this context"; return CPH_E_STATE; }
-  cph_status st = cph_exchange_energies(ctx, c.d.remd_rows);
-  return st ? st : cph_exchange_apply(ctx, c.d.remd_rows, seed, attempt);
+  cph_status st = sub_exchange_energies(ctx, c.d.remd_rows);
+  return st ? st : sub_exchange_apply(ctx, c.d.remd_rows, seed, attempt);
 }
 
-cph_status cph_get_labels(cph_ctx *ctx, int32_t *labels) {
+static cph_status sub_get_labels(SubCtx *ctx, int32_t *labels) {
   if (!ctx || !labels) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = need_remd(c);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   CK(cudaMemcpy(labels, c.d.remd_label, sizeof(int) * c.kp.R, cudaMemcpyDeviceToHost));
   return CPH_OK;
 }
 
-cph_status cph_set_labels(cph_ctx *ctx, const int32_t *labels) {
+static cph_status sub_set_labels(SubCtx *ctx, const int32_t *labels) {
   CPH_NVTX("cph_set_labels");
   if (!ctx || !labels) return CPH_E_INVALID;
   Ctx &c = ctx->c;
@@ -1368,18 +1366,18 @@ cph_status cph_set_labels(cph_ctx *ctx, const int32_t *labels) {
   return check_flags(c);
 }
 
-cph_status cph_get_exchange_stats(cph_ctx *ctx, int64_t *attempts, int64_t *accepts) {
+static cph_status sub_get_exchange_stats(SubCtx *ctx, int64_t *attempts, int64_t *accepts) {
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = need_remd(c);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   const size_t n = (size_t)(c.kp.remd_total / c.kp.P) * (c.kp.P - 1);
   if (attempts) CK(cudaMemcpy(attempts, c.d.remd_att, sizeof(long long) * n, cudaMemcpyDeviceToHost));
   if (accepts) CK(cudaMemcpy(accepts, c.d.remd_acc, sizeof(long long) * n, cudaMemcpyDeviceToHost));
   return CPH_OK;
 }
 
-cph_status cph_get_dbo_params(cph_ctx *ctx, int32_t r, double *p) {
+static cph_status sub_get_dbo_params(SubCtx *ctx, int32_t r, double *p) {
   if (!ctx || !p) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
@@ -1388,7 +1386,7 @@ cph_status cph_get_dbo_params(cph_ctx *ctx, int32_t r, double *p) {
   return CPH_OK;
 }
 
-cph_status cph_set_dbo_params(cph_ctx *ctx, int32_t r, const double *p) {
+static cph_status sub_set_dbo_params(SubCtx *ctx, int32_t r, const double *p) {
   CPH_NVTX("cph_set_dbo_params");
   if (!ctx || !p) return CPH_E_INVALID;
   Ctx &c = ctx->c;
@@ -1413,33 +1411,23 @@ cph_status cph_set_dbo_params(cph_ctx *ctx, int32_t r, const double *p) {
   return check_flags(c);
 }
 
-cph_status cph_get_dbo_events(cph_ctx *ctx, cph_dbo_event *ev, int64_t cap, int64_t *n) {
-  if (!ctx || cap < 0 || (cap > 0 && !ev)) return CPH_E_INVALID;
-  Ctx &c = ctx->c;
-  const int64_t take = std::min<int64_t>(cap, (int64_t)c.events.size());
-  std::copy(c.events.begin(), c.events.begin() + take, ev);
-  c.events.erase(c.events.begin(), c.events.begin() + take);
-  if (n) *n = take;
-  return CPH_OK;
-}
-
-cph_status cph_get_dbo_stats(cph_ctx *ctx, int32_t r, double *well, double *barrier) {
+static cph_status sub_get_dbo_stats(SubCtx *ctx, int32_t r, double *well, double *barrier) {
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   const size_t C = c.kp.C;
   if (well && C) CK(cudaMemcpy(well, c.d.dbo_well + r * C * 5, sizeof(double) * C * 5, cudaMemcpyDeviceToHost));
   if (barrier && C) CK(cudaMemcpy(barrier, c.d.dbo_bar + r * C * 4, sizeof(double) * C * 4, cudaMemcpyDeviceToHost));
   return CPH_OK;
 }
 
-cph_status cph_get_forces(cph_ctx *ctx, int32_t r, float *f, float *phi) {
+static cph_status sub_get_forces(SubCtx *ctx, int32_t r, float *f, float *phi) {
   CPH_NVTX("cph_get_forces");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   const KParams &kp = c.kp;
   const size_t N = kp.N, base = (size_t)r * kp.Nst;
   std::vector<float4> nb(N), rec(N), xq(N);
@@ -1474,12 +1462,12 @@ cph_status cph_get_forces(cph_ctx *ctx, int32_t r, float *f, float *phi) {
   return CPH_OK;
 }
 
-cph_status cph_get_positions(cph_ctx *ctx, int32_t r, float *pos, float *vel) {
+static cph_status sub_get_positions(SubCtx *ctx, int32_t r, float *pos, float *vel) {
   CPH_NVTX("cph_get_positions");
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   const size_t N = c.kp.N, base = (size_t)r * c.kp.Nst;
   std::vector<float4> xq(N), v(N);
   std::vector<int2> meta(N);
@@ -1494,7 +1482,6 @@ cph_status cph_get_positions(cph_ctx *ctx, int32_t r, float *pos, float *vel) {
   return CPH_OK;
 }
 
-}  // extern "C"
 
 // Pair-list decoding for the getters (host side).  The device list of replica r is copied
 // once; row(slot) gives the original indices of every entry the pair kernel evaluates for
@@ -1541,15 +1528,14 @@ static cph_status decode_directed(Ctx &c, int r, std::vector<std::pair<int, int>
   return CPH_OK;
 }
 
-extern "C" {
 
-cph_status cph_get_pairlist_rows(cph_ctx *ctx, int32_t r, const int32_t *atoms, int32_t n_atoms, int32_t *row_ptr,
+static cph_status sub_get_pairlist_rows(SubCtx *ctx, int32_t r, const int32_t *atoms, int32_t n_atoms, int32_t *row_ptr,
                                  int32_t *cols, int64_t cap) {
   CPH_NVTX("cph_get_pairlist_rows");
   if (!ctx || !atoms || !row_ptr || n_atoms < 0 || cap < 0) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   for (int k = 0; k < n_atoms; ++k)
     if (atoms[k] < 0 || atoms[k] >= c.kp.N) { c.err = "atom index out of range"; return CPH_E_INVALID; }
   ListHost h;
@@ -1579,12 +1565,12 @@ static cph_status emit_pairs(std::vector<std::pair<int, int>> &out, int32_t *pai
   return CPH_OK;
 }
 
-cph_status cph_get_pairlist(cph_ctx *ctx, int32_t r, int32_t *pairs, int64_t cap, int64_t *n) {
+static cph_status sub_get_pairlist(SubCtx *ctx, int32_t r, int32_t *pairs, int64_t cap, int64_t *n) {
   CPH_NVTX("cph_get_pairlist");
   if (!ctx || !n) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   std::vector<std::pair<int, int>> all;
   if ((st = decode_directed(c, r, all))) return st;
   std::vector<std::pair<int, int>> out;
@@ -1593,23 +1579,23 @@ cph_status cph_get_pairlist(cph_ctx *ctx, int32_t r, int32_t *pairs, int64_t cap
   return emit_pairs(out, pairs, cap, n);
 }
 
-cph_status cph_get_pairlist_directed(cph_ctx *ctx, int32_t r, int32_t *pairs, int64_t cap, int64_t *n) {
+static cph_status sub_get_pairlist_directed(SubCtx *ctx, int32_t r, int32_t *pairs, int64_t cap, int64_t *n) {
   CPH_NVTX("cph_get_pairlist_directed");
   if (!ctx || !n) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   std::vector<std::pair<int, int>> all;
   if ((st = decode_directed(c, r, all))) return st;
   return emit_pairs(all, pairs, cap, n);
 }
 
-cph_status cph_get_lambda_groups(cph_ctx *ctx, int32_t r, int32_t *group_ptr, int32_t *coord_ptr, int32_t *atoms,
+static cph_status sub_get_lambda_groups(SubCtx *ctx, int32_t r, int32_t *group_ptr, int32_t *coord_ptr, int32_t *atoms,
                                  int32_t *slot_atoms) {
   if (!ctx || !group_ptr || !coord_ptr || !atoms || !slot_atoms) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   const KParams &kp = c.kp;
   const size_t N = kp.N, base = (size_t)r * kp.Nst;
   std::vector<int> iperm(N);
@@ -1635,11 +1621,11 @@ cph_status cph_get_lambda_groups(cph_ctx *ctx, int32_t r, int32_t *group_ptr, in
   return CPH_OK;
 }
 
-cph_status cph_get_ti_means(cph_ctx *ctx, int32_t r, double *mean, int64_t *n_samples) {
+static cph_status sub_get_ti_means(SubCtx *ctx, int32_t r, double *mean, int64_t *n_samples) {
   if (!ctx) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   long long n = 0;
   CK(cudaMemcpy(&n, c.d.ti_n, sizeof(long long), cudaMemcpyDeviceToHost));
   std::vector<double> s(c.kp.C);
@@ -1657,26 +1643,40 @@ static size_t state_bytes(const Ctx &c) {
 }
 
 static cph_status ensure_state_buf(Ctx &c) {
+  if (!c.h_bad) {
+    CK(cudaMallocHost(&c.h_bad, sizeof(int)));
+    *c.h_bad = 0;
+  }
   if (c.d.state_buf) return CPH_OK;
   c.d.state_buf = dalloc<char>(c, state_bytes(c) * c.kp.R);
   if (!c.d.state_buf) { c.err = "device allocation failed"; return CPH_E_OOM; }
   return CPH_OK;
 }
 
-// replicas [r0, r0 + nr) -> host blobs (packed on the device, one copy)
-static cph_status get_states(Ctx &c, int r0, int nr, void *buf) {
+// replicas [r0, r0 + nr) -> host blobs (packed on the device, one copy), enqueued; the caller
+// synchronises the stream before reading buf
+static cph_status get_states_enqueue(Ctx &c, int r0, int nr, void *buf) {
   cph_status st = ensure_state_buf(c);
   if (st) return st;
   const size_t one = state_bytes(c);
   c.launches += launch_pack_state(c, c.stream, c.d.state_buf, (long long)one, r0, nr, c.host_step);
   CK(cudaMemcpyAsync(buf, c.d.state_buf, one * nr, cudaMemcpyDeviceToHost, c.stream));
+  return CPH_OK;
+}
+
+static cph_status get_states(Ctx &c, int r0, int nr, void *buf) {
+  cph_status st = get_states_enqueue(c, r0, nr, buf);
+  if (st) return st;
   CK(cudaStreamSynchronize(c.stream));
   return CPH_OK;
 }
 
-// host blobs -> replicas [r0, r0 + nr): headers checked on the host, finiteness on the device
-// before anything is overwritten; then TI restart and a fresh evaluation
-static cph_status set_states(Ctx &c, int r0, int nr, const void *buf, int64_t nbytes) {
+// host blobs -> replicas [r0, r0 + nr), in three stages so that several sub-batches can run
+// them side by side: (1) headers checked on the host, the blobs uploaded and checked for
+// finiteness on the device (flag read back into pinned c.h_bad); (2) after a stream sync,
+// reject a non-finite state before anything is overwritten; (3) unpack, move the clock, restart
+// the TI accumulators and evaluate the new configuration (enqueued).
+static cph_status set_states_begin(Ctx &c, int r0, int nr, const void *buf, int64_t nbytes, int64_t *step_out) {
   const size_t one = state_bytes(c);
   if (nbytes < (int64_t)(one * nr)) { c.err = "state blob too small"; return CPH_E_INVALID; }
   int64_t blob_step = -1;
@@ -1706,30 +1706,44 @@ static cph_status set_states(Ctx &c, int r0, int nr, const void *buf, int64_t nb
   if (st) return st;
   CK(cudaMemcpyAsync(c.d.state_buf, buf, one * nr, cudaMemcpyHostToDevice, c.stream));
   c.launches += launch_check_state(c, c.stream, c.d.state_buf, (long long)one, nr);
-  int bad = 0;
-  CK(cudaMemcpyAsync(&bad, c.d.flags + FLAG_BAD_STATE, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  CK(cudaStreamSynchronize(c.stream));
-  if (bad) {
-    const int zero = 0;
-    CK(cudaMemcpy(c.d.flags + FLAG_BAD_STATE, &zero, sizeof(int), cudaMemcpyHostToDevice));
-    c.err = "non-finite state";
-    return CPH_E_INVALID;
-  }
+  CK(cudaMemcpyAsync(c.h_bad, c.d.flags + FLAG_BAD_STATE, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  *step_out = blob_step;
+  return CPH_OK;
+}
+
+static cph_status set_states_rejected(Ctx &c) {
+  if (!*c.h_bad) return CPH_OK;
+  *c.h_bad = 0;
+  const int zero = 0;
+  CK(cudaMemcpy(c.d.flags + FLAG_BAD_STATE, &zero, sizeof(int), cudaMemcpyHostToDevice));
+  c.err = "non-finite state";
+  return CPH_E_INVALID;
+}
+
+static cph_status set_states_apply(Ctx &c, int r0, int nr, int64_t blob_step) {
+  const size_t one = state_bytes(c);
   c.launches += launch_unpack_state(c, c.stream, c.d.state_buf, (long long)one, r0, nr);
-  if (all && blob_step != c.host_step) {
+  if (r0 == 0 && nr == c.kp.R && blob_step != c.host_step) {
     c.host_step = blob_step;
-    const long long st64 = blob_step;
-    CK(cudaMemcpyAsync(c.d.step, &st64, sizeof(long long), cudaMemcpyHostToDevice, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
+    k_set_end<<<1, 1, 0, c.stream>>>(c.d.step, blob_step);
+    c.launches += 1;
   }
   // a new configuration: TI accumulators restart
   CK(cudaMemsetAsync(c.d.ti_sum, 0, sizeof(double) * (size_t)c.kp.R * c.kp.C, c.stream));
   CK(cudaMemsetAsync(c.d.ti_n, 0, sizeof(long long), c.stream));
-  if ((st = evaluate_here(c))) return st;
+  return evaluate_here(c);
+}
+
+static cph_status set_states(Ctx &c, int r0, int nr, const void *buf, int64_t nbytes) {
+  int64_t step = 0;
+  cph_status st = set_states_begin(c, r0, nr, buf, nbytes, &step);
+  if (st) return st;
+  CK(cudaStreamSynchronize(c.stream));
+  if ((st = set_states_rejected(c)) || (st = set_states_apply(c, r0, nr, step))) return st;
   return check_flags(c);
 }
 
-cph_status cph_get_state(cph_ctx *ctx, int32_t r, void *buf, int64_t cap, int64_t *n) {
+static cph_status sub_get_state(SubCtx *ctx, int32_t r, void *buf, int64_t cap, int64_t *n) {
   CPH_NVTX("cph_get_state");
   if (!ctx || !n) return CPH_E_INVALID;
   Ctx &c = ctx->c;
@@ -1739,20 +1753,20 @@ cph_status cph_get_state(cph_ctx *ctx, int32_t r, void *buf, int64_t cap, int64_
   if (!buf) return CPH_OK;
   if (cap < *n) { c.err = "state buffer too small"; return CPH_E_INVALID; }
   cudaSetDevice(c.device);
-  if ((st = cph_sync(ctx))) return st;
+  if ((st = sub_sync(ctx))) return st;
   return get_states(c, r, 1, buf);
 }
 
-cph_status cph_set_state(cph_ctx *ctx, int32_t r, const void *buf, int64_t nbytes) {
+static cph_status sub_set_state(SubCtx *ctx, int32_t r, const void *buf, int64_t nbytes) {
   CPH_NVTX("cph_set_state");
   if (!ctx || !buf) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cph_status st = check_replica(c, r);
-  if (st || (st = cph_sync(ctx))) return st;
+  if (st || (st = sub_sync(ctx))) return st;
   return set_states(c, r, 1, buf, nbytes);
 }
 
-cph_status cph_get_state_all(cph_ctx *ctx, void *buf, int64_t cap, int64_t *n) {
+static cph_status sub_get_state_all(SubCtx *ctx, void *buf, int64_t cap, int64_t *n) {
   CPH_NVTX("cph_get_state_all");
   if (!ctx || !n) return CPH_E_INVALID;
   Ctx &c = ctx->c;
@@ -1760,79 +1774,612 @@ cph_status cph_get_state_all(cph_ctx *ctx, void *buf, int64_t cap, int64_t *n) {
   if (!buf) return CPH_OK;
   if (cap < *n) { c.err = "state buffer too small"; return CPH_E_INVALID; }
   cudaSetDevice(c.device);
-  cph_status st = cph_sync(ctx);
+  cph_status st = sub_sync(ctx);
   if (st) return st;
   return get_states(c, 0, c.kp.R, buf);
 }
 
-cph_status cph_set_state_all(cph_ctx *ctx, const void *buf, int64_t nbytes) {
+static cph_status sub_set_state_all(SubCtx *ctx, const void *buf, int64_t nbytes) {
   CPH_NVTX("cph_set_state_all");
   if (!ctx || !buf) return CPH_E_INVALID;
   Ctx &c = ctx->c;
   cudaSetDevice(c.device);
-  cph_status st = cph_sync(ctx);
+  cph_status st = sub_sync(ctx);
   if (st) return st;
   return set_states(c, 0, c.kp.R, buf, nbytes);
 }
 
-cph_status cph_profile_steps(cph_ctx *ctx, int64_t n_steps, double *ms, int64_t *launches) {
-  CPH_NVTX("cph_profile_steps");
-  if (!ctx || n_steps < 0) return CPH_E_INVALID;
-  Ctx &c = ctx->c;
+// Eager steps of every sub-batch with CUDA events around each kernel class on `main`: per step
+// and class, the sub-batches' launches of that class run concurrently on their own streams
+// (fork from / join to `main`), so a class time is that of the kernel over the whole batch, as
+// in the stepped graph, not of S smaller serialised launches.  Classes are serialised.
+static cph_status profile_batches(const std::vector<Ctx *> &cs, const std::vector<cudaStream_t> &ss,
+                                  cudaStream_t main, int64_t n_steps, double *ms, int64_t *launches) {
+  Ctx &c = *cs[0];
   cudaSetDevice(c.device);
-  cudaStream_t s = c.stream;
-  std::vector<cudaEvent_t> evs;
+  const size_t S = cs.size();
+  std::vector<cudaEvent_t> evs, joins(S, nullptr);
   std::vector<int> cls;
+  cudaEvent_t fork = nullptr;
+  CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  for (auto &e : joins) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   static const char *kClassNames[] = {"integrate", "pairlist", "nonbonded", "spread", "fft_r2c", "solve",
                                       "fft_c2r", "gather", "lambda", "hi"};
   auto mark = [&](int k) {
     if (k >= 0 && k < (int)(sizeof(kClassNames) / sizeof(kClassNames[0]))) nvtxMarkA(kClassNames[k]);
     cudaEvent_t e;
     cudaEventCreate(&e);
-    cudaEventRecord(e, s);
+    cudaEventRecord(e, main);
     evs.push_back(e);
     cls.push_back(k);
   };
   int64_t cnt[CPH_N_KCLASSES] = {0};
+  // one kernel class over every sub-batch, concurrently; returns launches
+  auto phase = [&](int k, auto &&fn) {
+    cudaEventRecord(fork, main);
+    for (size_t b = 0; b < S; ++b)
+      if (ss[b] != main) cudaStreamWaitEvent(ss[b], fork, 0);
+    int q = 0;
+    for (size_t b = 0; b < S; ++b) q += fn(*cs[b], ss[b]);
+    for (size_t b = 0; b < S; ++b)
+      if (ss[b] != main) {
+        cudaEventRecord(joins[b], ss[b]);
+        cudaStreamWaitEvent(main, joins[b], 0);
+      }
+    if (k >= 0) cnt[k] += q;
+    cs[0]->launches += q;
+    mark(k);
+  };
   const long long end = c.host_step + n_steps;
-  k_set_end<<<1, 1, 0, s>>>(c.d.end_step, end);
-  int k = 1;
   mark(-1);
-  k += launch_lambda_open(c, s); cnt[CPH_K_LAMBDA] += 1;
-  mark(CPH_K_LAMBDA);
-  cufftSetStream(c.plan_r2c, s);
-  cufftSetStream(c.plan_c2r, s);
-  while (c.host_step < end) {
-    const bool rebuild = (c.host_step + 1) % c.kp.nstlist == 0;
-    { int q = launch_integrate(c, s, 1); k += q; cnt[CPH_K_INTEGRATE] += q; mark(CPH_K_INTEGRATE); }
-    if (rebuild) { int q = launch_rebuild(c, s); k += q; cnt[CPH_K_PAIRLIST] += q; mark(CPH_K_PAIRLIST); }
-    { int q = launch_nonbonded(c, s, 1); k += q; cnt[CPH_K_NONBONDED] += q; mark(CPH_K_NONBONDED); }
-    { int q = launch_spread(c, s); k += q; cnt[CPH_K_SPREAD] += q; mark(CPH_K_SPREAD); }
-    cufftExecR2C(c.plan_r2c, c.d.grid, (cufftComplex *)c.d.cgrid); mark(CPH_K_FFT_R2C);
-    k += launch_solve(c, s, 1); cnt[CPH_K_SOLVE] += 1; mark(CPH_K_SOLVE);
-    cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid); mark(CPH_K_FFT_C2R);
-    k += launch_gather(c, s); cnt[CPH_K_GATHER] += 1; mark(CPH_K_GATHER);
-    if (c.kp.hi) {
-      int q = launch_hi_recip(c, s) + launch_hi_finish(c, s, 1);
-      k += q; cnt[CPH_K_HI] += q; mark(CPH_K_HI);
-    }
-    k += launch_lambda_reduce(c, s, 1); cnt[CPH_K_LAMBDA] += 1; mark(CPH_K_LAMBDA);
-    c.host_step += 1;
+  phase(CPH_K_LAMBDA, [&](Ctx &x, cudaStream_t s) {
+    k_set_end<<<1, 1, 0, s>>>(x.d.end_step, end);
+    cufftSetStream(x.plan_r2c, s);
+    cufftSetStream(x.plan_c2r, s);
+    return 1 + launch_lambda_open(x, s);
+  });
+  cnt[CPH_K_LAMBDA] -= (int64_t)S;   // k_set_end is not a lambda kernel
+  long long t = c.host_step;
+  while (t < end) {
+    const bool rebuild = (t + 1) % c.kp.nstlist == 0;
+    phase(CPH_K_INTEGRATE, [&](Ctx &x, cudaStream_t s) { return launch_integrate(x, s, 1); });
+    if (rebuild) phase(CPH_K_PAIRLIST, [&](Ctx &x, cudaStream_t s) { return launch_rebuild(x, s); });
+    phase(CPH_K_NONBONDED, [&](Ctx &x, cudaStream_t s) { return launch_nonbonded(x, s, 1); });
+    phase(CPH_K_SPREAD, [&](Ctx &x, cudaStream_t s) { return launch_spread(x, s); });
+    phase(CPH_K_FFT_R2C, [&](Ctx &x, cudaStream_t) {
+      cufftExecR2C(x.plan_r2c, x.d.grid, (cufftComplex *)x.d.cgrid);
+      return 0;
+    });
+    phase(CPH_K_SOLVE, [&](Ctx &x, cudaStream_t s) { return launch_solve(x, s, 1); });
+    phase(CPH_K_FFT_C2R, [&](Ctx &x, cudaStream_t) {
+      cufftExecC2R(x.plan_c2r, (cufftComplex *)x.d.cgrid, x.d.grid);
+      return 0;
+    });
+    phase(CPH_K_GATHER, [&](Ctx &x, cudaStream_t s) { return launch_gather(x, s); });
+    if (c.kp.hi)
+      phase(CPH_K_HI, [&](Ctx &x, cudaStream_t s) { return launch_hi_recip(x, s) + launch_hi_finish(x, s, 1); });
+    phase(CPH_K_LAMBDA, [&](Ctx &x, cudaStream_t s) { return launch_lambda_reduce(x, s, 1); });
+    ++t;
   }
-  k += launch_close(c, s, 1); cnt[CPH_K_INTEGRATE] += 1; mark(CPH_K_INTEGRATE);
-  c.launches += k;
-  CK(cudaStreamSynchronize(s));
+  phase(CPH_K_INTEGRATE, [&](Ctx &x, cudaStream_t s) { return launch_close(x, s, 1); });
+  for (Ctx *x : cs) x->host_step = end;
+  CK(cudaStreamSynchronize(main));
   double acc[CPH_N_KCLASSES] = {0};
   for (size_t e = 1; e < evs.size(); ++e) {
-    float t = 0.f;
-    cudaEventElapsedTime(&t, evs[e - 1], evs[e]);
-    acc[cls[e]] += t;
+    float tm = 0.f;
+    cudaEventElapsedTime(&tm, evs[e - 1], evs[e]);
+    acc[cls[e]] += tm;
   }
   for (auto e : evs) cudaEventDestroy(e);
+  for (auto e : joins) cudaEventDestroy(e);
+  cudaEventDestroy(fork);
   if (ms) for (int q = 0; q < CPH_N_KCLASSES; ++q) ms[q] = acc[q];
   if (launches) for (int q = 0; q < CPH_N_KCLASSES; ++q) launches[q] = cnt[q];
   CK(cudaGetLastError());
-  return check_flags(c);
+  for (Ctx *x : cs)
+    if (cph_status st = check_flags(*x)) {
+      if (x != &c) c.err = x->err;
+      return st;
+    }
+  return CPH_OK;
+}
+
+// ---- public API: a context = S replica sub-batches stepped concurrently ----------------------
+// Each sub-batch is a complete single-batch context (SubCtx above) over a consecutive replica
+// range with its own stream; with S > 1 the caller's stream forks into the sub-batch streams
+// and joins back around every enqueuing call, so the public ordering contract (everything on
+// cph_get_stream) is unchanged.  cph_step interleaves the sub-batches block by block: the
+// PME chain of one batch (FFTs, solve, gather, lambda reduction: a few hundred CTAs at
+// most) then overlaps the other batch's pair kernel instead of idling SMs at every step end
+// (profiles/r02_summary.md).
+struct cph_ctx {
+  std::vector<SubCtx *> sub;
+  std::vector<int> first;          // local replica index of each sub-batch's replica 0
+  int R = 0, P = 0, remd_total = 0, nstlist = 1;
+  int device = 0;
+  cudaStream_t stream = nullptr;   // the public stream
+  bool own_stream = false;
+  std::vector<cudaStream_t> sstream;
+  cudaEvent_t ev_in = nullptr;
+  std::vector<cudaEvent_t> ev_out;
+  double *rows = nullptr;          // cph_exchange scratch (S > 1)
+  std::vector<cph_dbo_event> events;
+  std::string err;
+};
+
+__global__ void k_spin(long long ns) {
+  unsigned long long start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
+  for (;;) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if ((long long)(now - start) >= ns) break;
+    __nanosleep(1000);
+  }
+}
+
+namespace {
+
+cph_status fwd(cph_ctx *ctx, int s, cph_status st) {
+  if (st != CPH_OK) ctx->err = ctx->sub[s]->c.err;
+  return st;
+}
+
+// sub-batch holding local replica r, and its index there
+int locate(cph_ctx *ctx, int r, int *rl) {
+  if (r < 0 || r >= ctx->R) {
+    ctx->err = "replica index out of range";
+    return -1;
+  }
+  int s = (int)ctx->sub.size() - 1;
+  while (ctx->first[s] > r) --s;
+  *rl = r - ctx->first[s];
+  return s;
+}
+
+// order the sub-batch streams after / before the public stream (no-ops for S = 1)
+cph_status fork_in(cph_ctx *ctx) {
+  if (ctx->sub.size() < 2) return CPH_OK;
+  cudaSetDevice(ctx->device);
+  if (cudaEventRecord(ctx->ev_in, ctx->stream) != cudaSuccess) { ctx->err = "cudaEventRecord failed"; return CPH_E_CUDA; }
+  for (cudaStream_t s : ctx->sstream)
+    if (cudaStreamWaitEvent(s, ctx->ev_in, 0) != cudaSuccess) { ctx->err = "cudaStreamWaitEvent failed"; return CPH_E_CUDA; }
+  return CPH_OK;
+}
+
+cph_status join_out(cph_ctx *ctx) {
+  if (ctx->sub.size() < 2) return CPH_OK;
+  cudaSetDevice(ctx->device);
+  for (size_t s = 0; s < ctx->sstream.size(); ++s)
+    if (cudaEventRecord(ctx->ev_out[s], ctx->sstream[s]) != cudaSuccess ||
+        cudaStreamWaitEvent(ctx->stream, ctx->ev_out[s], 0) != cudaSuccess) {
+      ctx->err = "stream join failed";
+      return CPH_E_CUDA;
+    }
+  return CPH_OK;
+}
+
+void destroy_composite(cph_ctx *ctx) {
+  for (SubCtx *s : ctx->sub) sub_destroy(s);
+  cudaSetDevice(ctx->device);
+  if (ctx->rows) cudaFree(ctx->rows);
+  for (cudaStream_t s : ctx->sstream) cudaStreamDestroy(s);
+  for (cudaEvent_t e : ctx->ev_out) cudaEventDestroy(e);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int level_of(const cph_params *prm, double pH) {
+  for (int p = 0; p < prm->n_ph_levels; ++p)
+    if (std::fabs(pH - prm->ph_levels[p]) <= 1e-9 * std::max(1.0, std::fabs(prm->ph_levels[p]))) return p;
+  return -1;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *cph_last_error(const cph_ctx *ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **out) {
+  CPH_NVTX("cph_create");
+  if (!out) { g_create_err = "out is NULL"; return CPH_E_INVALID; }
+  *out = nullptr;
+  if (!sys || !prm) { g_create_err = "system/params is NULL"; return CPH_E_INVALID; }
+  if (prm->abi_version != CPH_ABI_VERSION) { g_create_err = "abi_version mismatch"; return CPH_E_INVALID; }
+  const int R = prm->n_replicas;
+  if (R < 1) { g_create_err = "n_replicas must be >= 1"; return CPH_E_INVALID; }
+  if (prm->sub_batches < 0) { g_create_err = "sub_batches must be >= 0"; return CPH_E_INVALID; }
+  // automatic: up to 4 batches once the whole batch holds >= 24k atoms (measured on B200 over
+  // C1..C5 x 2..64 replicas: 4 to 19 % less time per step; below that size the
+  // step is launch-bound and extra batches only add launches)
+  int S = prm->sub_batches ? prm->sub_batches : ((int64_t)R * sys->n_atoms >= 24000 ? 4 : 1);
+  S = std::min(S, R);
+  if (const char *e = getenv("CPH_SUB_BATCHES")) S = std::max(1, std::min(R, atoi(e)));   // A/B override
+  // a ladder split across sub-batches is checked here (each sub-batch checks the ladders it
+  // holds whole); a pH outside the levels is reported by the sub-batch
+  if (S > 1 && prm->n_ph_levels >= 2 && prm->ph_levels && prm->pH) {
+    std::vector<int> lab(R);
+    bool all = true;
+    for (int r = 0; r < R; ++r) all = all && (lab[r] = level_of(prm, prm->pH[r])) >= 0;
+    if (all && !labels_form_ladders(lab.data(), R, prm->remd_first, prm->n_ph_levels)) {
+      g_create_err = "each pH ladder held by this context must carry every level exactly once";
+      return CPH_E_INVALID;
+    }
+  }
+  cph_ctx *ctx = new cph_ctx;
+  ctx->R = R;
+  ctx->P = prm->n_ph_levels;
+  ctx->remd_total = prm->remd_total ? prm->remd_total : R;
+  ctx->nstlist = std::max(1, prm->nstlist);
+  ctx->device = prm->device;
+  auto fail = [&](cph_status st, const std::string &m) {
+    g_create_err = m;
+    destroy_composite(ctx);
+    return st;
+  };
+  if (S == 1) {
+    SubCtx *s0 = nullptr;
+    cph_params p1 = *prm;
+    p1.sub_batches = 1;
+    cph_status st = sub_create(sys, &p1, &s0);
+    if (st) { delete ctx; return st; }   // g_create_err set by sub_create
+    ctx->sub.push_back(s0);
+    ctx->first.push_back(0);
+    ctx->stream = s0->c.stream;
+    *out = ctx;
+    return CPH_OK;
+  }
+  if (cudaSetDevice(prm->device) != cudaSuccess) return fail(CPH_E_CUDA, "cudaSetDevice failed");
+  if (prm->cuda_stream) ctx->stream = (cudaStream_t)prm->cuda_stream;
+  else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(CPH_E_CUDA, "stream creation failed");
+    ctx->own_stream = true;
+  }
+  if (cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess)
+    return fail(CPH_E_CUDA, "event creation failed");
+  int C = 0, N = sys->n_atoms, off = 0;
+  for (int s = 0; s < S; ++s) {
+    const int Rs = R / S + (s < R % S ? 1 : 0);
+    cudaStream_t st_s = nullptr;
+    cudaEvent_t ev = nullptr;
+    if (cudaStreamCreateWithFlags(&st_s, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(CPH_E_CUDA, "stream creation failed");
+    ctx->sstream.push_back(st_s);
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+      return fail(CPH_E_CUDA, "event creation failed");
+    ctx->ev_out.push_back(ev);
+    cph_params ps = *prm;
+    ps.n_replicas = Rs;
+    ps.sub_batches = 1;
+    ps.cuda_stream = st_s;
+    if (prm->pH) ps.pH = prm->pH + off;
+    if (prm->replica_seed) ps.replica_seed = prm->replica_seed + off;
+    if (prm->lambda0) ps.lambda0 = prm->lambda0 + (size_t)off * C;   // C known after batch 0 (off = 0 there)
+    if (prm->pos_replicas) ps.pos_replicas = prm->pos_replicas + (size_t)off * N * 3;
+    if (prm->vel_replicas) ps.vel_replicas = prm->vel_replicas + (size_t)off * N * 3;
+    if (prm->n_ph_levels) {
+      ps.remd_first = prm->remd_first + off;
+      ps.remd_total = ctx->remd_total;
+    }
+    SubCtx *sc = nullptr;
+    cph_status st = sub_create(sys, &ps, &sc);
+    if (st) return fail(st, g_create_err);
+    ctx->sub.push_back(sc);
+    ctx->first.push_back(off);
+    C = sc->c.kp.C;
+    off += Rs;
+  }
+  if (ctx->P && ctx->remd_total == R) {
+    if (cudaMalloc(&ctx->rows, sizeof(double) * (size_t)R * (ctx->P + 1)) != cudaSuccess)
+      return fail(CPH_E_CUDA, "cudaMalloc failed");
+  }
+  // the sub-batches evaluated step 0 on their own streams: order the public stream after them
+  if (join_out(ctx)) return fail(CPH_E_CUDA, ctx->err);
+  *out = ctx;
+  return CPH_OK;
+}
+
+void cph_destroy(cph_ctx *ctx) {
+  if (!ctx) return;
+  destroy_composite(ctx);
+}
+
+void *cph_get_stream(const cph_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+int32_t cph_n_coords(const cph_ctx *ctx) { return ctx ? sub_n_coords(ctx->sub[0]) : -1; }
+int32_t cph_n_atoms(const cph_ctx *ctx) { return ctx ? sub_n_atoms(ctx->sub[0]) : -1; }
+int32_t cph_n_replicas(const cph_ctx *ctx) { return ctx ? ctx->R : -1; }
+int32_t cph_n_sub_batches(const cph_ctx *ctx) { return ctx ? (int32_t)ctx->sub.size() : -1; }
+int64_t cph_current_step(const cph_ctx *ctx) { return ctx ? sub_current_step(ctx->sub[0]) : -1; }
+int64_t cph_launch_count(const cph_ctx *ctx) {
+  if (!ctx) return -1;
+  int64_t n = 0;
+  for (SubCtx *s : ctx->sub) n += sub_launch_count(s);
+  return n;
+}
+
+cph_status cph_step(cph_ctx *ctx, int64_t n_steps) {
+  CPH_NVTX("cph_step");
+  if (!ctx) return CPH_E_INVALID;
+  if (n_steps < 0) { ctx->err = "n_steps < 0"; return CPH_E_INVALID; }
+  if (n_steps == 0) return CPH_OK;
+  if (ctx->sub.size() == 1) return fwd(ctx, 0, sub_step(ctx->sub[0], n_steps));
+  cph_status st = fork_in(ctx);
+  if (st) return st;
+  static const long long stagger_us = getenv("CPH_SUB_STAGGER_US") ? atoll(getenv("CPH_SUB_STAGGER_US")) : 0;
+  if (stagger_us > 0)
+    for (size_t s = 1; s < ctx->sub.size(); ++s) k_spin<<<1, 1, 0, ctx->sstream[s]>>>(stagger_us * (long long)s * 1000);
+  // interleave the sub-batches in chunks of 32 nstlist blocks (aligned to the rebuild phase, so
+  // full blocks replay the captured graphs): long enough that the per-segment cost (the
+  // k_close / k_lambda_open pair and a graph launch that can no longer be pipelined behind
+  // the previous one, ~0.1-0.3 ms measured) is rare, short enough that a long cph_step call
+  // keeps every sub-batch stream fed instead of filling the launch queue with one of them
+  static const long long chunk_blocks = getenv("CPH_SUB_CHUNK") ? atoll(getenv("CPH_SUB_CHUNK")) : 32;
+  const long long chunk = chunk_blocks > 0 ? chunk_blocks * ctx->nstlist : n_steps;
+  long long t = sub_current_step(ctx->sub[0]);
+  const long long end = t + n_steps;
+  while (t < end) {
+    const long long next = std::min<long long>(end, (t / ctx->nstlist) * ctx->nstlist + chunk);
+    for (size_t s = 0; s < ctx->sub.size(); ++s)
+      if ((st = fwd(ctx, (int)s, sub_step(ctx->sub[s], next - t)))) return st;
+    t = next;
+  }
+  return join_out(ctx);
+}
+
+cph_status cph_sync(cph_ctx *ctx) {
+  CPH_NVTX("cph_sync");
+  if (!ctx) return CPH_E_INVALID;
+  for (size_t s = 0; s < ctx->sub.size(); ++s)
+    if (cph_status st = fwd(ctx, (int)s, sub_sync(ctx->sub[s]))) return st;
+  if (ctx->sub.size() > 1 && cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    ctx->err = "cudaStreamSynchronize failed";
+    return CPH_E_CUDA;
+  }
+  return CPH_OK;
+}
+
+// per-replica calls: route to the sub-batch; enqueuing ones fork / join around the call
+#define CPH_ROUTE(call_expr, enqueues)                                  \
+  if (!ctx) return CPH_E_INVALID;                                     \
+  int rl = 0;                                                         \
+  const int s = locate(ctx, r, &rl);                                  \
+  if (s < 0) return CPH_E_INVALID;                                    \
+  SubCtx *sc = ctx->sub[s];                                           \
+  if (enqueues) { if (cph_status e0 = fork_in(ctx)) return e0; }      \
+  cph_status st_ = fwd(ctx, s, call_expr);                            \
+  if (enqueues) { if (cph_status e1 = join_out(ctx)) return e1; }     \
+  return st_;
+
+cph_status cph_set_pH(cph_ctx *ctx, int32_t r, double pH) { CPH_ROUTE(sub_set_pH(sc, rl, pH), true) }
+cph_status cph_get_lambdas(cph_ctx *ctx, int32_t r, double *lam, double *vel) {
+  CPH_ROUTE(sub_get_lambdas(sc, rl, lam, vel), false)
+}
+cph_status cph_get_dvdl(cph_ctx *ctx, int32_t r, double *coul, double *bias) {
+  CPH_ROUTE(sub_get_dvdl(sc, rl, coul, bias), false)
+}
+cph_status cph_get_bias_params(cph_ctx *ctx, int32_t r, double *d1) { CPH_ROUTE(sub_get_bias_params(sc, rl, d1), false) }
+cph_status cph_get_energies(cph_ctx *ctx, int32_t r, double *e) { CPH_ROUTE(sub_get_energies(sc, rl, e), false) }
+cph_status cph_get_frames_ex(cph_ctx *ctx, int32_t r, float *buf, uint8_t *censored, int64_t *steps, int32_t *labels,
+                             int64_t cap, int64_t *n_frames, int64_t *n_dropped) {
+  CPH_ROUTE(sub_get_frames_ex(sc, rl, buf, censored, steps, labels, cap, n_frames, n_dropped), false)
+}
+cph_status cph_get_frames(cph_ctx *ctx, int32_t r, float *buf, int64_t cap, int64_t *n_frames, int64_t *n_dropped) {
+  CPH_ROUTE(sub_get_frames(sc, rl, buf, cap, n_frames, n_dropped), false)
+}
+cph_status cph_get_dbo_params(cph_ctx *ctx, int32_t r, double *p) { CPH_ROUTE(sub_get_dbo_params(sc, rl, p), false) }
+cph_status cph_set_dbo_params(cph_ctx *ctx, int32_t r, const double *p) {
+  CPH_ROUTE(sub_set_dbo_params(sc, rl, p), true)
+}
+cph_status cph_get_dbo_stats(cph_ctx *ctx, int32_t r, double *well, double *barrier) {
+  CPH_ROUTE(sub_get_dbo_stats(sc, rl, well, barrier), false)
+}
+cph_status cph_get_forces(cph_ctx *ctx, int32_t r, float *f, float *phi) { CPH_ROUTE(sub_get_forces(sc, rl, f, phi), false) }
+cph_status cph_get_positions(cph_ctx *ctx, int32_t r, float *pos, float *vel) {
+  CPH_ROUTE(sub_get_positions(sc, rl, pos, vel), false)
+}
+cph_status cph_get_pairlist_rows(cph_ctx *ctx, int32_t r, const int32_t *atoms, int32_t n_atoms, int32_t *row_ptr,
+                                 int32_t *cols, int64_t cap) {
+  CPH_ROUTE(sub_get_pairlist_rows(sc, rl, atoms, n_atoms, row_ptr, cols, cap), false)
+}
+cph_status cph_get_pairlist(cph_ctx *ctx, int32_t r, int32_t *pairs, int64_t cap, int64_t *n) {
+  CPH_ROUTE(sub_get_pairlist(sc, rl, pairs, cap, n), false)
+}
+cph_status cph_get_pairlist_directed(cph_ctx *ctx, int32_t r, int32_t *pairs, int64_t cap, int64_t *n) {
+  CPH_ROUTE(sub_get_pairlist_directed(sc, rl, pairs, cap, n), false)
+}
+cph_status cph_get_lambda_groups(cph_ctx *ctx, int32_t r, int32_t *group_ptr, int32_t *coord_ptr, int32_t *atoms,
+                                 int32_t *slot_atoms) {
+  CPH_ROUTE(sub_get_lambda_groups(sc, rl, group_ptr, coord_ptr, atoms, slot_atoms), false)
+}
+cph_status cph_get_ti_means(cph_ctx *ctx, int32_t r, double *mean, int64_t *n_samples) {
+  CPH_ROUTE(sub_get_ti_means(sc, rl, mean, n_samples), false)
+}
+cph_status cph_get_state(cph_ctx *ctx, int32_t r, void *buf, int64_t cap, int64_t *n) {
+  CPH_ROUTE(sub_get_state(sc, rl, buf, cap, n), false)
+}
+cph_status cph_set_state(cph_ctx *ctx, int32_t r, const void *buf, int64_t nbytes) {
+  CPH_ROUTE(sub_set_state(sc, rl, buf, nbytes), true)
+}
+#undef CPH_ROUTE
+
+cph_status cph_exchange_energies(cph_ctx *ctx, double *rows) {
+  if (!ctx || !rows) return CPH_E_INVALID;
+  cph_status st = fork_in(ctx);
+  if (st) return st;
+  for (size_t s = 0; s < ctx->sub.size(); ++s)
+    if ((st = fwd(ctx, (int)s, sub_exchange_energies(ctx->sub[s], rows + (size_t)ctx->first[s] * (ctx->P + 1)))))
+      return st;
+  return join_out(ctx);
+}
+
+cph_status cph_exchange_apply(cph_ctx *ctx, const double *rows_all, uint64_t seed, int64_t attempt) {
+  if (!ctx) return CPH_E_INVALID;
+  cph_status st = fork_in(ctx);
+  if (st) return st;
+  for (size_t s = 0; s < ctx->sub.size(); ++s)
+    if ((st = fwd(ctx, (int)s, sub_exchange_apply(ctx->sub[s], rows_all, seed, attempt)))) return st;
+  return join_out(ctx);
+}
+
+cph_status cph_exchange(cph_ctx *ctx, uint64_t seed, int64_t attempt) {
+  if (!ctx) return CPH_E_INVALID;
+  if (ctx->sub.size() == 1) return fwd(ctx, 0, sub_exchange(ctx->sub[0], seed, attempt));
+  if (!ctx->P) { ctx->err = "replica exchange is off (n_ph_levels = 0)"; return CPH_E_STATE; }
+  if (!ctx->rows) { ctx->err = "cph_exchange needs every replica in this context"; return CPH_E_STATE; }
+  // energies of every sub-batch are joined into the public stream before any apply forks
+  cph_status st = cph_exchange_energies(ctx, ctx->rows);
+  return st ? st : cph_exchange_apply(ctx, ctx->rows, seed, attempt);
+}
+
+cph_status cph_get_labels(cph_ctx *ctx, int32_t *labels) {
+  if (!ctx || !labels) return CPH_E_INVALID;
+  for (size_t s = 0; s < ctx->sub.size(); ++s)
+    if (cph_status st = fwd(ctx, (int)s, sub_get_labels(ctx->sub[s], labels + ctx->first[s]))) return st;
+  return CPH_OK;
+}
+
+cph_status cph_set_labels(cph_ctx *ctx, const int32_t *labels) {
+  if (!ctx || !labels) return CPH_E_INVALID;
+  if (ctx->P && ctx->sub.size() > 1) {
+    for (int r = 0; r < ctx->R; ++r)
+      if (labels[r] < 0 || labels[r] >= ctx->P) { ctx->err = "label out of range"; return CPH_E_INVALID; }
+    if (!labels_form_ladders(labels, ctx->R, ctx->sub[0]->c.kp.remd_first, ctx->P)) {
+      ctx->err = "each pH ladder held by this context must carry every level exactly once";
+      return CPH_E_INVALID;
+    }
+  }
+  cph_status st = fork_in(ctx);
+  if (st) return st;
+  for (size_t s = 0; s < ctx->sub.size(); ++s)
+    if ((st = fwd(ctx, (int)s, sub_set_labels(ctx->sub[s], labels + ctx->first[s])))) return st;
+  return join_out(ctx);
+}
+
+cph_status cph_get_exchange_stats(cph_ctx *ctx, int64_t *attempts, int64_t *accepts) {
+  if (!ctx) return CPH_E_INVALID;
+  // every sub-batch applies every ladder's decisions and counts them: batch 0's tally is the one
+  for (size_t s = 1; s < ctx->sub.size(); ++s)
+    if (cph_status st = fwd(ctx, (int)s, sub_sync(ctx->sub[s]))) return st;
+  return fwd(ctx, 0, sub_get_exchange_stats(ctx->sub[0], attempts, accepts));
+}
+
+cph_status cph_get_dbo_events(cph_ctx *ctx, cph_dbo_event *ev, int64_t cap, int64_t *n) {
+  if (!ctx || cap < 0 || (cap > 0 && !ev)) return CPH_E_INVALID;
+  // drain every sub-batch, map to local replica indices, merge in (step, replica) order
+  bool added = false;
+  for (size_t s = 0; s < ctx->sub.size(); ++s) {
+    std::vector<cph_dbo_event> &q = ctx->sub[s]->c.events;
+    for (cph_dbo_event e : q) {
+      e.replica += ctx->first[s];
+      ctx->events.push_back(e);
+      added = true;
+    }
+    q.clear();
+  }
+  if (added)
+    std::stable_sort(ctx->events.begin(), ctx->events.end(), [](const cph_dbo_event &a, const cph_dbo_event &b) {
+      return a.step != b.step ? a.step < b.step : a.replica < b.replica;
+    });
+  const int64_t take = std::min<int64_t>(cap, (int64_t)ctx->events.size());
+  std::copy(ctx->events.begin(), ctx->events.begin() + take, ev);
+  ctx->events.erase(ctx->events.begin(), ctx->events.begin() + take);
+  if (n) *n = take;
+  return CPH_OK;
+}
+
+cph_status cph_get_state_all(cph_ctx *ctx, void *buf, int64_t cap, int64_t *n) {
+  CPH_NVTX("cph_get_state_all");
+  if (!ctx || !n) return CPH_E_INVALID;
+  if (ctx->sub.size() == 1) return fwd(ctx, 0, sub_get_state_all(ctx->sub[0], buf, cap, n));
+  const int64_t one = (int64_t)state_bytes(ctx->sub[0]->c);
+  *n = one * ctx->R;
+  if (!buf) return CPH_OK;
+  if (cap < *n) { ctx->err = "state buffer too small"; return CPH_E_INVALID; }
+  cudaSetDevice(ctx->device);
+  // latched errors first; then every sub-batch packs and copies out side by side
+  for (size_t s = 0; s < ctx->sub.size(); ++s)
+    if (cph_status st = fwd(ctx, (int)s, sub_sync(ctx->sub[s]))) return st;
+  for (size_t s = 0; s < ctx->sub.size(); ++s) {
+    Ctx &c = ctx->sub[s]->c;
+    if (cph_status st = fwd(ctx, (int)s, get_states_enqueue(c, 0, c.kp.R, (char *)buf + one * ctx->first[s])))
+      return st;
+  }
+  for (size_t s = 0; s < ctx->sub.size(); ++s)
+    if (cudaStreamSynchronize(ctx->sub[s]->c.stream) != cudaSuccess) {
+      ctx->err = "cudaStreamSynchronize failed";
+      return CPH_E_CUDA;
+    }
+  return CPH_OK;
+}
+
+cph_status cph_set_state_all(cph_ctx *ctx, const void *buf, int64_t nbytes) {
+  CPH_NVTX("cph_set_state_all");
+  if (!ctx || !buf) return CPH_E_INVALID;
+  if (ctx->sub.size() == 1) return fwd(ctx, 0, sub_set_state_all(ctx->sub[0], buf, nbytes));
+  const size_t S = ctx->sub.size();
+  const int64_t one = (int64_t)state_bytes(ctx->sub[0]->c);
+  if (nbytes < one * ctx->R) { ctx->err = "state blob too small"; return CPH_E_INVALID; }
+  cudaSetDevice(ctx->device);
+  // every header is checked (all blobs one step) before any sub-batch is touched
+  const Ctx &c0 = ctx->sub[0]->c;
+  int64_t step0 = -1;
+  for (int r = 0; r < ctx->R; ++r) {
+    int64_t hdr[4];
+    std::memcpy(hdr, (const char *)buf + one * r, sizeof hdr);
+    if (hdr[0] != kMagic || hdr[1] != (int64_t)c0.kp.N || hdr[2] != (int64_t)c0.kp.C) {
+      ctx->err = "state blob does not match this context";
+      return CPH_E_INVALID;
+    }
+    if (hdr[3] < 0 || (r > 0 && hdr[3] != step0)) {
+      ctx->err = "state blobs carry different (or negative) steps";
+      return CPH_E_INVALID;
+    }
+    step0 = hdr[3];
+  }
+  cph_status st;
+  for (size_t s = 0; s < S; ++s)
+    if ((st = fwd(ctx, (int)s, sub_sync(ctx->sub[s])))) return st;
+  if ((st = fork_in(ctx))) return st;
+  // upload + finiteness check on every sub-batch; nothing is overwritten unless all pass
+  std::vector<int64_t> steps(S);
+  for (size_t s = 0; s < S; ++s) {
+    Ctx &c = ctx->sub[s]->c;
+    if ((st = fwd(ctx, (int)s, set_states_begin(c, 0, c.kp.R, (const char *)buf + one * ctx->first[s],
+                                                 one * c.kp.R, &steps[s]))))
+      return st;
+  }
+  cph_status rejected = CPH_OK;
+  for (size_t s = 0; s < S; ++s) {
+    Ctx &c = ctx->sub[s]->c;
+    if (cudaStreamSynchronize(c.stream) != cudaSuccess) { ctx->err = "cudaStreamSynchronize failed"; return CPH_E_CUDA; }
+    if (cph_status r = set_states_rejected(c)) { if (!rejected) { rejected = r; ctx->err = c.err; } }
+  }
+  if (rejected) return rejected;
+  for (size_t s = 0; s < S; ++s) {
+    Ctx &c = ctx->sub[s]->c;
+    if ((st = fwd(ctx, (int)s, set_states_apply(c, 0, c.kp.R, steps[s])))) return st;
+  }
+  for (size_t s = 0; s < S; ++s)
+    if ((st = fwd(ctx, (int)s, check_flags(ctx->sub[s]->c)))) return st;
+  return join_out(ctx);
+}
+
+cph_status cph_profile_steps(cph_ctx *ctx, int64_t n_steps, double *ms, int64_t *launches) {
+  CPH_NVTX("cph_profile_steps");
+  if (!ctx || n_steps < 0) return CPH_E_INVALID;
+  std::vector<Ctx *> cs;
+  std::vector<cudaStream_t> ss;
+  for (SubCtx *s : ctx->sub) {
+    cs.push_back(&s->c);
+    ss.push_back(s->c.stream);
+  }
+  cph_status st = fork_in(ctx);
+  if (st) return st;
+  if ((st = fwd(ctx, 0, profile_batches(cs, ss, ctx->stream, n_steps, ms, launches)))) return st;
+  return join_out(ctx);
 }
 
 }  // extern "C"

@@ -75,7 +75,7 @@ def test_dbo_defaults_are_the_papers(cph):
     import ctypes
     p = cph.binding.cph_params()
     cph.lib().cph_default_params(ctypes.byref(p))
-    assert p.abi_version == 3 and p.deterministic == 0 and p.dbo_well == 0 and p.dbo_barrier == 0
+    assert p.abi_version == 4 and p.deterministic == 0 and p.sub_batches == 0 and p.dbo_well == 0 and p.dbo_barrier == 0
     assert (p.dbo_well_steps, p.dbo_barrier_steps, p.dbo_censor_steps) == (20000, 500000, 5000)   # 40 ps, 1 ns, 10 ps
     assert (p.dbo_well_near, p.dbo_residency, p.dbo_well_tol, p.dbo_well_gain, p.dbo_well_cap) == (0.2, 0.7, 0.03, 0.5, 0.08)
     assert (p.dbo_trans_lo, p.dbo_trans_hi, p.dbo_target, p.dbo_target_tol) == (0.2, 0.8, 0.25, 0.05)
@@ -109,4 +109,19 @@ def test_replica_exchange_ladders_must_be_permutations(cph, labels):
     levels = [4.0, 5.0, 6.0]
     with pytest.raises(cph.CphError) as ei:
         cph.cph_create(s, [levels[k] for k in labels], [1, 2, 3], ph_levels=levels, use_torch_allocator=False)
+    assert ei.value.status == 1 and "ladder" in str(ei.value)
+
+
+def test_sub_batches_validated(cph):
+    """cph_params.sub_batches: negative is an error; a pH ladder split across two replica
+    sub-batches is checked as a whole by the context (each sub-batch sees only part of it)."""
+    s = _sys()
+    with pytest.raises(cph.CphError) as ei:
+        cph.cph_create(s, [4.0], [1], sub_batches=-1, use_torch_allocator=False)
+    assert ei.value.status == 1 and "sub_batches" in str(ei.value)
+    levels = [4.0, 5.0]
+    # R = 4 in 3 sub-batches (2, 1, 1): ladder 1 = replicas 2, 3 spans batches 1 and 2
+    with pytest.raises(cph.CphError) as ei:
+        cph.cph_create(s, [4.0, 5.0, 5.0, 5.0], [1, 2, 3, 4], ph_levels=levels, sub_batches=3,
+                       use_torch_allocator=False)
     assert ei.value.status == 1 and "ladder" in str(ei.value)
