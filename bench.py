@@ -364,7 +364,7 @@ def main():
         ent = tr.get("entries", {}).get(f"{s.name}/R{R}", {}).get(dom)
         if ent is not None:
             traffic = ent
-            traffic_src = (f"profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum per launch from "
+            traffic_src = (f"profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum per whole-batch launch from "
                            f"one ncu --set full capture ({tr.get('captured', '?')}), not measured in this run")
     except Exception:
         pass
