@@ -11,6 +11,8 @@
 // sectors per lane and a warp of the pair kernel reads 1 KB contiguous per 8 neighbours.
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "cph_device.cuh"
 
 namespace cph {
@@ -431,10 +433,18 @@ __device__ __forceinline__ bool canonical_in_code(float4 xj, float4 xi, float3 L
 // columns (raw xy offsets -2..2 with their uniform periodic images) the warp's union z window
 // [min(z_i - R_i), max(z_i + R_i)], R_i = sqrt(r_list'^2 - d_xy,i^2), selects the column's
 // cells (plus the image run when the window crosses z = 0 or L); their atoms are staged 32 at
-// a time in shared memory and each lane tests them with the image-staged fast d^2, the exact
-// canonical decision (R14, image included) inside the rounding band, and appends
-// accepted entries to its 16-entry shared-memory ring, flushed as whole 32-byte list tiles.
+// a time in shared memory (structure of arrays, image shift applied) and each lane tests them
+// four at a time: the fast d^2 with paired FP32 ops (FADD2 / FMUL2 / FFMA2: the roundings of
+// the scalar formula), one warp-level test for a candidate inside the rounding band of
+// r_list^2 (those get the exact canonical decision, R14, image included), and
+// predicated appends to the lane's 16-entry shared-memory ring in candidate order, flushed as
+// whole 32-byte list tiles.  Warps holding an atom with excluded pairs run the same loop with
+// the exclusion test compiled in.  (A 64-entry ring flushed once per staged chunk needed 64 KB
+// of shared memory per CTA, which shrank the L1 of the pair kernels co-running from other
+// replica sub-batches: step +10 %.)
 constexpr int kColWarps = 8;
+constexpr int kStage = 36;      // staged candidates per warp: 32 + sentinel padding for aligned groups of 4
+constexpr int kRing = 16;       // per-lane ring: <= 4 accepted per group + 7 pending
 
 __global__ void __launch_bounds__(32 * kColWarps) k_build_list_col(KParams kp, DevBufs d) {
   const int r = blockIdx.y, colid = blockIdx.x;
@@ -450,14 +460,21 @@ __global__ void __launch_bounds__(32 * kColWarps) k_build_list_col(KParams kp, D
   const float3 Linv = make_float3(kp.invL[0], kp.invL[1], kp.invL[2]);
   const float rlist2 = kp.rlist2;
   const float lo2 = kp.rlist2 * (1.0f - 3e-5f), hi2 = kp.rlist2 * (1.0f + 3e-5f);
+  // conservative band test |d^2 - mid| <= hw (a superset of [lo2, hi2): the margin covers the
+  // rounding of d^2 - mid); non-band candidates are accepted iff d^2 < lo2, as in the band rule
+  const float2 nmid = make_float2(-0.5f * (lo2 + hi2), -0.5f * (lo2 + hi2));
+  const float hw = 0.5f * (hi2 - lo2) * 1.01f;
   const float csx = kp.L[0] / (float)kp.nc[0], csy = kp.L[1] / (float)kp.nc[1], csz = kp.L[2] / (float)nz;
   const float win_r = sqrtf(kp.rlist2) * 1.0001f + kWinPad;
   const float win_r2 = win_r * win_r;
   __shared__ int s_colc[25], s_code[25];
   __shared__ float s_sx[25], s_sy[25], s_xlo[25], s_ylo[25];
-  __shared__ float4 s_pos[kColWarps][32];
-  __shared__ int s_ent[kColWarps][32];
-  __shared__ uint32_t s_ring[kColWarps][16][32];
+  // staged candidates, structure of arrays (float2 pairs feed the paired FP32 ops), padded to
+  // 36 with far-away sentinels so groups of 4 never need an index clamp
+  __shared__ __align__(16) float s_px[kColWarps][kStage], s_py[kColWarps][kStage], s_pz[kColWarps][kStage];
+  __shared__ __align__(16) int s_ent[kColWarps][kStage];
+  __shared__ int s_org[kColWarps][kStage];
+  __shared__ uint32_t s_ring[kColWarps * kRing * 32];
   if (threadIdx.x < 25) {
     const int k = c_walk[threadIdx.x * 5] / 5;            // column ring order around the centre
     const int rx = cx - 2 + k / 5, ry = cy - 2 + k % 5;
@@ -470,9 +487,14 @@ __global__ void __launch_bounds__(32 * kColWarps) k_build_list_col(KParams kp, D
     s_code[threadIdx.x] = (1 - wx) * 9 + (1 - wy) * 3;
   }
   __syncthreads();
-  float4 *sx = s_pos[w];
-  int *sj = s_ent[w];
-  uint32_t (*s_buf)[32] = s_ring[w];
+  float *px = s_px[w], *py = s_py[w], *pz = s_pz[w];
+  int *sj = s_ent[w], *so = s_org[w];
+  if (lane < kStage - 32) {
+    px[32 + lane] = py[32 + lane] = pz[32 + lane] = 1e30f;
+    sj[32 + lane] = 0;
+    so[32 + lane] = -1;
+  }
+  uint32_t *ring = s_ring + w * kRing * 32 + lane;      // entry k at ring[(k & 15) * 32]
   uint32_t *nbl = d.nbl + (size_t)r * kp.cap * kp.Nst;
   for (int i0 = cb + 32 * w; i0 < ce; i0 += 32 * kColWarps) {
     const int i = i0 + lane;
@@ -480,9 +502,72 @@ __global__ void __launch_bounds__(32 * kColWarps) k_build_list_col(KParams kp, D
     const float4 xi = valid ? xq[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     const int orig = valid ? meta[i].x : 0;
     const int eb = valid ? d.excl_ptr[orig] : 0, ee = valid ? d.excl_ptr[orig + 1] : 0;
+    const bool warp_excl = __any_sync(0xffffffffu, ee > eb);
+    const float2 nxi = make_float2(-xi.x, -xi.x), nyi = make_float2(-xi.y, -xi.y), nzi = make_float2(-xi.z, -xi.z);
     uint4 *out = reinterpret_cast<uint4 *>(nbl) + 2 * (size_t)(valid ? i : 0);
     const size_t ostride = 2 * (size_t)kp.Nst;
     int cnt = 0, flushed = 0;
+    auto excluded = [&](int oj) {
+      bool ex = false;
+      for (int e = eb; e < ee; ++e) ex |= (d.excl_idx[e] == oj);
+      return ex;
+    };
+    // test the staged slice [tb, te) four candidates at a time (EXCL: exclusion test compiled in)
+    auto scan = [&](auto excl_tag, int tb, int te, int tself, int fast_code) {
+      constexpr bool EXCL = decltype(excl_tag)::value;
+      for (int t0 = tb & ~3; t0 < te; t0 += 4) {
+        const float4 x4 = *reinterpret_cast<const float4 *>(px + t0);
+        const float4 y4 = *reinterpret_cast<const float4 *>(py + t0);
+        const float4 z4 = *reinterpret_cast<const float4 *>(pz + t0);
+        const int4 e4 = *reinterpret_cast<const int4 *>(sj + t0);
+        const int ev[4] = {e4.x, e4.y, e4.z, e4.w};
+        const float2 xa = make_float2(x4.x, x4.y), xb = make_float2(x4.z, x4.w);
+        const float2 ya = make_float2(y4.x, y4.y), yb = make_float2(y4.z, y4.w);
+        const float2 za = make_float2(z4.x, z4.y), zb = make_float2(z4.z, z4.w);
+        const float2 dxa = __fadd2_rn(xa, nxi), dxb = __fadd2_rn(xb, nxi);
+        const float2 dya = __fadd2_rn(ya, nyi), dyb = __fadd2_rn(yb, nyi);
+        const float2 dza = __fadd2_rn(za, nzi), dzb = __fadd2_rn(zb, nzi);
+        const float2 qa = __ffma2_rn(dxa, dxa, __ffma2_rn(dya, dya, __fmul2_rn(dza, dza)));
+        const float2 qb = __ffma2_rn(dxb, dxb, __ffma2_rn(dyb, dyb, __fmul2_rn(dzb, dzb)));
+        const float2 ma = __fadd2_rn(qa, nmid), mb = __fadd2_rn(qb, nmid);
+        const float d2[4] = {qa.x, qa.y, qb.x, qb.y};
+        if (!(fminf(fminf(fabsf(ma.x), fabsf(ma.y)), fminf(fabsf(mb.x), fabsf(mb.y))) <= hw)) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            bool ok = d2[u] < lo2 && t0 + u != tself;
+            if (EXCL && ok && ee > eb) ok = !excluded(so[t0 + u]);
+            if (ok) {
+              ring[(cnt & (kRing - 1)) * 32] = (uint32_t)ev[u];
+              ++cnt;
+            }
+          }
+        } else {                                 // rare: a candidate near r_list^2
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (!(d2[u] < hi2)) continue;
+            const int je = ev[u];
+            const int j = je & (int)kEntryJMask;
+            if (!(d2[u] < lo2)) {
+              int cc;
+              if (!canonical_in_code(xq[j], xi, Lbox, Linv, rlist2, &cc) || cc != fast_code) continue;
+            }
+            if (j == i) continue;
+            if (EXCL && ee > eb && excluded(so[t0 + u])) continue;
+            ring[(cnt & (kRing - 1)) * 32] = (uint32_t)je;
+            ++cnt;
+          }
+        }
+        if (cnt - flushed >= 8) {                // flush a whole 32-byte tile
+          if (flushed < kp.cap) {
+            const uint32_t *t = ring + (flushed & (kRing - 1)) * 32;
+            out[0] = make_uint4(t[0], t[32], t[64], t[96]);
+            out[1] = make_uint4(t[128], t[160], t[192], t[224]);
+            out += ostride;
+          }
+          flushed += 8;
+        }
+      }
+    };
     for (int q = 0; q < 25; ++q) {
       const float xlo = s_xlo[q], ylo = s_ylo[q];
       const float ddx = fmaxf(0.f, fmaxf(xlo - xi.x, xi.x - (xlo + csx + 2.f * kWinPad)));
@@ -527,53 +612,23 @@ __global__ void __launch_bounds__(32 * kColWarps) k_build_list_col(KParams kp, D
           float zt = 0.f;
           if (lane < nj) {
             const float4 p = xq[jb + lane];
-            sx[lane] = make_float4(p.x + wsx, p.y + wsy, p.z + wsz, 0.f);
-            sj[lane] = (jb + lane) | ((meta[jb + lane].y & (int)kEntryTypeMask) << kEntryTypeShift);
+            const int2 mt = meta[jb + lane];
+            px[lane] = p.x + wsx;
+            py[lane] = p.y + wsy;
+            pz[lane] = p.z + wsz;
+            sj[lane] = (jb + lane) | ((mt.y & (int)kEntryTypeMask) << kEntryTypeShift) | (fast_code << kEntryImgShift);
+            so[lane] = mt.x;
             zt = p.z;
+          } else {
+            px[lane] = py[lane] = pz[lane] = 1e30f;
           }
           // the staged atoms are z-sorted: the union window is a contiguous slice
           const int tb = __popc(__ballot_sync(0xffffffffu, lane < nj && zt < zwlo));
           const int te = __popc(__ballot_sync(0xffffffffu, lane < nj && zt <= zwhi));
           __syncwarp();
           if (!valid) continue;
-          for (int t0 = tb; t0 < te; t0 += 4) {
-            float d2v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float4 xj = sx[min(t0 + u, te - 1)];
-              const float dx = xj.x - xi.x, dy = xj.y - xi.y, dz = xj.z - xi.z;
-              d2v[u] = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              if (t0 + u >= te) continue;
-              if (d2v[u] >= hi2) continue;
-              const int je = sj[t0 + u] | (fast_code << kEntryImgShift);
-              const int j = je & (int)kEntryJMask;
-              if (d2v[u] >= lo2) {               // rounding band: exact canonical decision + image
-                int cc;
-                if (!canonical_in_code(xq[j], xi, Lbox, Linv, rlist2, &cc) || cc != fast_code) continue;
-              }
-              if (j == i) continue;
-              if (ee > eb) {                        // solute atoms only
-                const int oj = meta[j].x;
-                bool ex = false;
-                for (int e = eb; e < ee; ++e) ex |= (d.excl_idx[e] == oj);
-                if (ex) continue;
-              }
-              s_buf[cnt & 15][lane] = (uint32_t)je;
-              ++cnt;
-            }
-            if (cnt - flushed >= 8) {
-              if (flushed < kp.cap) {
-                const int h = flushed & 8;
-                out[0] = make_uint4(s_buf[h][lane], s_buf[h + 1][lane], s_buf[h + 2][lane], s_buf[h + 3][lane]);
-                out[1] = make_uint4(s_buf[h + 4][lane], s_buf[h + 5][lane], s_buf[h + 6][lane], s_buf[h + 7][lane]);
-                out += ostride;
-              }
-              flushed += 8;
-            }
-          }
+          if (warp_excl) scan(std::true_type{}, tb, te, i - jb, fast_code);
+          else scan(std::false_type{}, tb, te, i - jb, fast_code);
         }
       }
     }
@@ -581,10 +636,10 @@ __global__ void __launch_bounds__(32 * kColWarps) k_build_list_col(KParams kp, D
       // pad the last tile with the atom's own slot (zero shift, r = 0: skipped by the pair kernel)
       const uint32_t self = (uint32_t)i | ((uint32_t)(meta[i].y & (int)kEntryTypeMask) << kEntryTypeShift) |
                             (13u << kEntryImgShift);
-      const int h = flushed & 8;
-      for (int k = cnt - flushed; k < 8; ++k) s_buf[h + k][lane] = self;
-      out[0] = make_uint4(s_buf[h][lane], s_buf[h + 1][lane], s_buf[h + 2][lane], s_buf[h + 3][lane]);
-      out[1] = make_uint4(s_buf[h + 4][lane], s_buf[h + 5][lane], s_buf[h + 6][lane], s_buf[h + 7][lane]);
+      uint32_t *t = ring + (flushed & (kRing - 1)) * 32;
+      for (int k = cnt - flushed; k < 8; ++k) t[k * 32] = self;
+      out[0] = make_uint4(t[0], t[32], t[64], t[96]);
+      out[1] = make_uint4(t[128], t[160], t[192], t[224]);
     }
     if (valid) {
       d.nnb[base + i] = cnt;
