@@ -1907,17 +1907,6 @@ struct cph_ctx {
   std::string err;
 };
 
-__global__ void k_spin(long long ns) {
-  unsigned long long start;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
-  for (;;) {
-    unsigned long long now;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    if ((long long)(now - start) >= ns) break;
-    __nanosleep(1000);
-  }
-}
-
 namespace {
 
 cph_status fwd(cph_ctx *ctx, int s, cph_status st) {
@@ -2108,9 +2097,6 @@ cph_status cph_step(cph_ctx *ctx, int64_t n_steps) {
   if (ctx->sub.size() == 1) return fwd(ctx, 0, sub_step(ctx->sub[0], n_steps));
   cph_status st = fork_in(ctx);
   if (st) return st;
-  static const long long stagger_us = getenv("CPH_SUB_STAGGER_US") ? atoll(getenv("CPH_SUB_STAGGER_US")) : 0;
-  if (stagger_us > 0)
-    for (size_t s = 1; s < ctx->sub.size(); ++s) k_spin<<<1, 1, 0, ctx->sstream[s]>>>(stagger_us * (long long)s * 1000);
   // interleave the sub-batches in chunks of 32 nstlist blocks (aligned to the rebuild phase, so
   // full blocks replay the captured graphs): long enough that the per-segment cost (the
   // k_close / k_lambda_open pair and a graph launch that can no longer be pipelined behind
