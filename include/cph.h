@@ -199,7 +199,9 @@ typedef struct {
    * are those of one batch up to rounding (identical trajectories in tests/test_gpu_subbatch.py).
    * Automatic: S = min(R, 4) when R * n_atoms >= 24000, else 1.  Every call
    * stays ordered on cph_get_stream(); per-replica getters route to the batch holding the
-   * replica. */
+   * replica.  A call that fails part-way (e.g. a latched device error during cph_step) can
+   * leave the batches at different steps: restore a checkpoint (cph_set_state_all) or
+   * destroy the context. */
   int32_t sub_batches;
 } cph_params;
 

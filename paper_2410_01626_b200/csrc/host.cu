@@ -1902,7 +1902,7 @@ struct cph_ctx {
   std::vector<cudaStream_t> sstream;
   cudaEvent_t ev_in = nullptr;
   std::vector<cudaEvent_t> ev_out;
-  double *rows = nullptr;          // cph_exchange scratch (S > 1)
+  double *rows = nullptr;          // cph_exchange scratch (S > 1; freed with batch 0)
   std::vector<cph_dbo_event> events;
   std::string err;
 };
@@ -1951,7 +1951,6 @@ cph_status join_out(cph_ctx *ctx) {
 void destroy_composite(cph_ctx *ctx) {
   for (SubCtx *s : ctx->sub) sub_destroy(s);
   cudaSetDevice(ctx->device);
-  if (ctx->rows) cudaFree(ctx->rows);
   for (cudaStream_t s : ctx->sstream) cudaStreamDestroy(s);
   for (cudaEvent_t e : ctx->ev_out) cudaEventDestroy(e);
   if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
@@ -2061,9 +2060,9 @@ cph_status cph_create(const cph_system *sys, const cph_params *prm, cph_ctx **ou
     C = sc->c.kp.C;
     off += Rs;
   }
-  if (ctx->P && ctx->remd_total == R) {
-    if (cudaMalloc(&ctx->rows, sizeof(double) * (size_t)R * (ctx->P + 1)) != cudaSuccess)
-      return fail(CPH_E_CUDA, "cudaMalloc failed");
+  if (ctx->P && ctx->remd_total == R) {   // cph_exchange scratch, owned by batch 0's allocations
+    ctx->rows = dalloc<double>(ctx->sub[0]->c, (size_t)R * (ctx->P + 1));
+    if (!ctx->rows) return fail(CPH_E_OOM, "device allocation failed");
   }
   // the sub-batches evaluated step 0 on their own streams: order the public stream after them
   if (join_out(ctx)) return fail(CPH_E_CUDA, ctx->err);
