@@ -375,6 +375,15 @@ def main():
             "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" if dk.get("unit") == "TFLOP/s"
             else f"MEASURED_PEAKS.json hbm_gbs ({hbm_kind})"}
 
+    # whole-step roofline: the pair flops at the FP32 peak plus the spread,
+    # gather, two FFTs, solve and integrator bytes at the HBM peak, for all R replicas
+    t_roof_ms = 1e3 * (alg["nonbonded_flop"] / (FP32_PEAK_TFLOPS * 1e12) +
+                       (alg["spread_bytes"] + alg["gather_bytes"] + 2.0 * alg["fft_bytes_each"] +
+                        alg["solve_bytes"] + alg["integrate_bytes"]) / (hbm * 1e9))
+    step_roof = {"t_roof_ms": t_roof_ms, "frac": t_roof_ms / ms_step,
+                 "definition": "SURVEY 8(d): R x (60 flop x P_rc at the FP32 peak + spread/gather/FFT/solve/"
+                               "integrator algorithmic bytes at the HBM peak) / measured ms per step"}
+
     # e2e through the public API with host buffers: per step, the whole replica state is
     # uploaded from pinned host memory (cph_set_state_all: positions, velocities, lambdas;
     # forces re-evaluated at the uploaded state), one cph_step, and the new state read back
@@ -436,7 +445,7 @@ def main():
         "ns_per_day_per_system": ns_day_system, "lambda_steps_per_s_per_system": steps_per_s,
         "lambda_coord_updates_per_s": steps_per_s * s.n_coords * R * world,
         "clocks": clocks, "gpu_launches": launches,
-        "roofline": roof, "kernels": kernels, "extra": extra,
+        "roofline": roof, "step_roofline": step_roof, "kernels": kernels, "extra": extra,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(blob.size) * world,
                 "d2h_bytes_per_step": int(blob.size) * world, "steps": E,
