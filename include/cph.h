@@ -371,7 +371,10 @@ cph_status cph_get_state(cph_ctx *ctx, int32_t replica, void *buf, int64_t cap, 
 cph_status cph_set_state(cph_ctx *ctx, int32_t replica, const void *buf, int64_t n);
 
 /* All replicas at once (blob = R consecutive per-replica blobs of cph_get_state);
- * cph_set_state_all re-evaluates forces once for the whole batch. */
+ * cph_set_state_all re-evaluates forces once for the whole batch.  A restore re-sorts the atoms
+ * and rebuilds the pair list unless every restored atom is where the last rebuild put it
+ * (minimum-image displacement <= 1e-5 nm): then that list is the list of the restored
+ * configuration and is kept. */
 cph_status cph_get_state_all(cph_ctx *ctx, void *buf, int64_t cap, int64_t *n);
 cph_status cph_set_state_all(cph_ctx *ctx, const void *buf, int64_t n);
 

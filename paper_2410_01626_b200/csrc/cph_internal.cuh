@@ -30,7 +30,7 @@ constexpr int kMaxAtoms = 1 << 21;
 
 // Device-side flags (int array)
 enum { FLAG_PENDING_CLOSE = 0, FLAG_LIST_OVERFLOW = 1, FLAG_DIVERGED = 2, FLAG_MAX_NNB = 3,
-       FLAG_STEP_DONE = 4, FLAG_BAD_STATE = 5, FLAG_REMD_BAD = 6, FLAG_COUNT = 8 };
+       FLAG_STEP_DONE = 4, FLAG_BAD_STATE = 5, FLAG_REMD_BAD = 6, FLAG_MOVED = 7, FLAG_COUNT = 8 };
 
 // Scalars every kernel needs, passed by value.
 struct KParams {
@@ -185,7 +185,7 @@ struct Ctx {
   std::vector<int> h_c_group, h_c_lp;               // [C]
   std::vector<long long> h_cens;                    // [R*G*2]
   std::vector<cph_dbo_event> events;                // undrained DBO log
-  int *h_bad = nullptr;                             // pinned: FLAG_BAD_STATE read back by set_state
+  int *h_bad = nullptr;                             // pinned [2]: FLAG_BAD_STATE, FLAG_MOVED read back by set_state
   std::vector<double> h_levels;                     // [P] pH ladder
   std::vector<double> h_lvl_d1, h_lvl_dG;           // [P*C], [P*G*3]
   DboConfig dbo;
@@ -223,6 +223,7 @@ int launch_hi_finish(Ctx &c, cudaStream_t s, int step_offset);
 int launch_pack_state(Ctx &c, cudaStream_t s, char *dst, long long one, int r0, int nr, long long step);
 int launch_check_state(Ctx &c, cudaStream_t s, const char *src, long long one, int nr);
 int launch_unpack_state(Ctx &c, cudaStream_t s, const char *src, long long one, int r0, int nr);
+int launch_list_moved(Ctx &c, cudaStream_t s, int r0, int nr);
 
 // host PFC (pfc.cu); dw = (a0, a1, h_prot, h_deprot) of each coordinate of the site
 bool pfc_two_state(const double dw[4], double pKa, double pH, double T, double kw, double *d1, std::string *err);

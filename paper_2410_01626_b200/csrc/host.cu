@@ -337,7 +337,10 @@ int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
 }
 
 // evaluation at the current state without integration (create / set_state)
-cph_status evaluate_here(Ctx &c) {
+// Forces, potentials and energies at the current state.  rebuild = false when the pair list of
+// the last rebuild is the list of the current positions (they have not moved since, or the
+// nstlist schedule covers them: a mid-run re-evaluation after a bias change).
+cph_status evaluate_here(Ctx &c, bool rebuild) {
   CPH_NVTX("evaluate_here");
   cudaStream_t s = c.stream;
   k_set_end<<<1, 1, 0, s>>>(c.d.end_step, c.host_step);
@@ -345,7 +348,7 @@ cph_status evaluate_here(Ctx &c) {
   CK(cudaMemsetAsync(c.d.bussi_k, 0, sizeof(double) * 2 * c.kp.R, s));
   int k = 1;
   k += launch_set_charges(c, s);
-  k += launch_rebuild(c, s);
+  if (rebuild) k += launch_rebuild(c, s);
   cufftSetStream(c.plan_r2c, s);
   cufftSetStream(c.plan_c2r, s);
   k += launch_spread(c, s);
@@ -976,7 +979,7 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   }
   c.host_step = 0;
   c.launches += launch_influence(c, c.stream);
-  cph_status st = evaluate_here(c);
+  cph_status st = evaluate_here(c, true);
   if (st == CPH_OK) st = check_flags(c);
   // a denser-than-average region overflowed the list capacity: grow it once (with margin)
   // and rebuild; an overflow during stepping is reported by the next call instead
@@ -994,7 +997,7 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
       return fail_create(ctx, CPH_E_CUDA);
     }
     c.err.clear();
-    st = evaluate_here(c);
+    st = evaluate_here(c, true);
     if (st == CPH_OK) st = check_flags(c);
   }
   if (st != CPH_OK) {
@@ -1168,7 +1171,7 @@ static cph_status dbo_block_end(Ctx &c) {
   if (cph_status st = run_pfc_many(c, reps, &changed_all)) return st;
   CK(cudaMemcpy(c.d.dw, c.h_dw.data(), sizeof(double) * c.h_dw.size(), cudaMemcpyHostToDevice));
   if (G) CK(cudaMemcpy(c.d.cens, c.h_cens.data(), sizeof(long long) * c.h_cens.size(), cudaMemcpyHostToDevice));
-  return evaluate_here(c);
+  return evaluate_here(c, false);          // block ends are multiples of nstlist: the list is fresh
 }
 
 static long long next_dbo_boundary(const Ctx &c) {
@@ -1407,7 +1410,7 @@ static cph_status sub_set_dbo_params(SubCtx *ctx, int32_t r, const double *p) {
   std::copy(p, p + (size_t)C * 4, c.h_dw.begin() + (size_t)r * C * 4);
   if (C) CK(cudaMemcpy(c.d.dw + (size_t)r * C * 4, p, sizeof(double) * C * 4, cudaMemcpyHostToDevice));
   if ((st = run_pfc(c, r))) return st;
-  if ((st = evaluate_here(c))) return st;
+  if ((st = evaluate_here(c, false))) return st;     // positions unchanged: the list stands
   return check_flags(c);
 }
 
@@ -1644,8 +1647,8 @@ static size_t state_bytes(const Ctx &c) {
 
 static cph_status ensure_state_buf(Ctx &c) {
   if (!c.h_bad) {
-    CK(cudaMallocHost(&c.h_bad, sizeof(int)));
-    *c.h_bad = 0;
+    CK(cudaMallocHost(&c.h_bad, 2 * sizeof(int)));
+    c.h_bad[0] = c.h_bad[1] = 0;
   }
   if (c.d.state_buf) return CPH_OK;
   c.d.state_buf = dalloc<char>(c, state_bytes(c) * c.kp.R);
@@ -1731,7 +1734,13 @@ static cph_status set_states_apply(Ctx &c, int r0, int nr, int64_t blob_step) {
   // a new configuration: TI accumulators restart
   CK(cudaMemsetAsync(c.d.ti_sum, 0, sizeof(double) * (size_t)c.kp.R * c.kp.C, c.stream));
   CK(cudaMemsetAsync(c.d.ti_n, 0, sizeof(long long), c.stream));
-  return evaluate_here(c);
+  // re-sort and rebuild unless every restored atom sits where the last rebuild put it (a
+  // restart of the configuration the list was built for, e.g. a checkpoint loop)
+  CK(cudaMemsetAsync(c.d.flags + FLAG_MOVED, 0, sizeof(int), c.stream));
+  c.launches += launch_list_moved(c, c.stream, r0, nr);
+  CK(cudaMemcpyAsync(c.h_bad + 1, c.d.flags + FLAG_MOVED, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  return evaluate_here(c, c.h_bad[1] != 0);
 }
 
 static cph_status set_states(Ctx &c, int r0, int nr, const void *buf, int64_t nbytes) {

@@ -69,6 +69,27 @@ __global__ void k_unpack_state(KParams kp, DevBufs d, const char *src, long long
   }
 }
 
+// FLAG_MOVED = 1 when an atom of replicas [r0, r0 + nr) is not where it was at the last
+// rebuild (xyzq_alt keeps the rebuild's wrapped positions until the next one): minimum-image
+// displacement above 1e-5 nm.  Otherwise the pair list built there is the list of this
+// configuration and a restore needs no re-sort and no rebuild.
+__global__ void k_list_moved(KParams kp, DevBufs d, int r0) {
+  const int r = r0 + blockIdx.y, s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= kp.N) return;
+  const size_t idx = (size_t)r * kp.Nst + s;
+  const float4 x = d.xyzq[idx], b = d.xyzq_alt[idx];
+  float dx = x.x - b.x, dy = x.y - b.y, dz = x.z - b.z;
+  dx -= kp.L[0] * rintf(dx * kp.invL[0]);
+  dy -= kp.L[1] * rintf(dy * kp.invL[1]);
+  dz -= kp.L[2] * rintf(dz * kp.invL[2]);
+  if (!(dx * dx + dy * dy + dz * dz <= 1e-10f)) d.flags[FLAG_MOVED] = 1;
+}
+
+int launch_list_moved(Ctx &c, cudaStream_t s, int r0, int nr) {
+  k_list_moved<<<dim3((c.kp.N + 255) / 256, nr), 256, 0, s>>>(c.kp, c.d, r0);
+  return 1;
+}
+
 int launch_pack_state(Ctx &c, cudaStream_t s, char *dst, long long one, int r0, int nr, long long step) {
   k_pack_state<<<dim3((c.kp.N + 255) / 256, nr), 256, 0, s>>>(c.kp, c.d, dst, one, r0, step);
   return 1;

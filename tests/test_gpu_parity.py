@@ -518,3 +518,30 @@ def test_deterministic_mode_bitwise_reproducible_and_parity(cph):
     for (xa, la), (xb, lb) in zip(runs[0], runs[1]):
         assert np.array_equal(xa[0], xb[0]) and np.array_equal(xa[1], xb[1])
         assert np.array_equal(la[0], lb[0]) and np.array_equal(la[1], lb[1])
+
+
+def test_restore_keeps_the_list_only_for_unmoved_atoms(cph):
+    """cph_set_state_all re-sorts and rebuilds the pair list unless every restored atom sits
+    where the last rebuild put it (then the list of the last rebuild is the list of this
+    configuration).  Moved atoms: the list is the canonical list at the restored positions;
+    a second restore of the same blob reuses it and gives bitwise the same forces."""
+    s = make_system(1)
+    ctx, *_ = _ctx(cph, s, 2, seed=4, deterministic=1)
+    ctx.cph_step(13)
+    blob = ctx.cph_get_state_all()
+    ctx.cph_step(7)                                   # the step-20 rebuild moves the list on
+    ctx.cph_set_state_all(blob)                       # restored atoms moved: rebuild
+    f1 = [ctx.cph_get_forces(r) for r in range(2)]
+    lists = []
+    for r in range(2):
+        x, _ = ctx.cph_get_positions(r)
+        got = ctx.cph_get_pairlist(r)
+        assert np.array_equal(got, OPL.canonical_pairs(x, s.box, s.params["rlist"], s.excl))
+        lists.append(got)
+    ctx.cph_step(3)                                   # no rebuild before step 19
+    ctx.cph_set_state_all(blob)                       # same positions as the list: reuse
+    for r in range(2):
+        f, phi = ctx.cph_get_forces(r)
+        assert np.array_equal(f, f1[r][0]) and np.array_equal(phi, f1[r][1])
+        assert np.array_equal(ctx.cph_get_pairlist(r), lists[r])
+    assert ctx.cph_current_step() == 13
