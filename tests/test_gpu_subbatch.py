@@ -189,3 +189,27 @@ def test_sub_batches_profile_and_default(cph):
     assert ctx.cph_current_step() == 10
     for r in range(R):
         np.testing.assert_allclose(ctx.cph_get_lambdas(r)[0], ref.cph_get_lambdas(r)[0], atol=1e-5)
+
+
+@pytest.mark.parametrize("variant", ["bussi", "hamiltonian", "ti"])
+def test_sub_batches_with_thermostat_hi_and_ti(cph, variant):
+    """The Bussi thermostat (per-replica kinetic-energy reductions), Hamiltonian interpolation
+    (per-group corrections) and fixed-lambda TI (per-replica accumulators) give one batch's
+    results in three sub-batches."""
+    s = make_system(1) if variant != "hamiltonian" else small_system()
+    R = 5
+    lam0, pH, seeds, vel = _inputs(s, R, 9)
+    kw = {"bussi": dict(thermostat="bussi"), "hamiltonian": dict(hamiltonian=1), "ti": dict(mode=1)}[variant]
+    out = []
+    for S in (1, 3):
+        ctx = cph.cph_create(s, pH, seeds, lambda0=lam0, vel_replicas=vel, deterministic=1, sub_batches=S, **kw)
+        ctx.cph_step(25)
+        snap = _snapshot(ctx, R)
+        ti = [ctx.cph_get_ti_means(r) for r in range(R)] if variant == "ti" else None
+        out.append((snap, ti))
+        ctx.close()
+    _assert_close(out[1][0], out[0][0])
+    if variant == "ti":
+        for (m1, n1), (m3, n3) in zip(out[0][1], out[1][1]):
+            assert n1 == n3 and n1 > 0
+            np.testing.assert_allclose(m3, m1, rtol=1e-6, atol=1e-9)
