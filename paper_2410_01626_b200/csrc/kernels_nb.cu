@@ -155,6 +155,13 @@ struct ShiftTab {
 // formulas and rounding as nb_atom (each packed op is the scalar op, element-wise).
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
+// address of the entry's neighbour: base + 16 * slot in one IMAD.WIDE.U32
+__device__ __forceinline__ const float4 *slot_ptr(const char *base, uint32_t e) {
+  const float4 *p;
+  asm("mad.wide.u32 %0, %1, 16, %2;" : "=l"(p) : "r"(e & kEntryJMask), "l"(base));
+  return p;
+}
+
 template <bool PHI64, bool SMALLT>
 __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, const float4 *__restrict__ xq,
                                            const float *__restrict__ c6n, const float *__restrict__ c12t,
@@ -181,8 +188,8 @@ __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, 
       if (t < kp.T) { r6n[t] = c6n[lrow + t]; r12[t] = c12t[lrow + t]; }
   }
   auto ljsel = [&](uint32_t e, float &v6, float &v12) {
-    const uint32_t t = (e >> kEntryTypeShift) & kEntryTypeMask;
-    const bool hi = t & 2u, od = t & 1u;
+    // the two type bits tested in place (one predicate-writing LOP3 each)
+    const bool hi = e & (2u << kEntryTypeShift), od = e & (1u << kEntryTypeShift);
     v6 = hi ? (od ? r6n[3] : r6n[2]) : (od ? r6n[1] : r6n[0]);
     v12 = hi ? (od ? r12[3] : r12[2]) : (od ? r12[1] : r12[0]);
   };
@@ -201,8 +208,8 @@ __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, 
   const char *xqb;
   asm("mov.b64 %0, %1;" : "=l"(xqb) : "l"(xq));
   auto pair = [&](uint32_t ea, uint32_t eb) {
-    const float4 xa = __ldg(reinterpret_cast<const float4 *>(xqb + (size_t)((ea & kEntryJMask) << 4)));
-    const float4 xb = __ldg(reinterpret_cast<const float4 *>(xqb + (size_t)((eb & kEntryJMask) << 4)));
+    const float4 xa = __ldg(slot_ptr(xqb, ea));
+    const float4 xb = __ldg(slot_ptr(xqb, eb));
     const float4 sa = shn.s[ea >> kEntryImgShift], sb = shn.s[eb >> kEntryImgShift];
     float2 c6, c12;                                                        // (-6 c6, 12 c12)
     if (SMALLT) {
