@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define CPH_ABI_VERSION 4
+#define CPH_ABI_VERSION 5
 
 typedef struct cph_ctx cph_ctx;
 
@@ -203,6 +203,19 @@ typedef struct {
    * leave the batches at different steps: restore a checkpoint (cph_set_state_all) or
    * destroy the context. */
   int32_t sub_batches;
+  /* Pair-list layout (ABI v5; 0 = automatic, the default).  1: a full per-atom Verlet list
+   * (every pair in both atoms' rows; the pair kernel sums each atom's row in a fixed order
+   * with no atomics).  2: a half cluster-pair list: super-clusters of 32 consecutive atoms of
+   * a cell column against j-clusters of 4 consecutive sorted atoms, each entry carrying one
+   * 32-bit interaction mask per 8-atom i-cluster whose bits are exactly the canonical pairs
+   * (R14, exclusions removed, each unordered pair once); the pair kernel evaluates
+   * a mask's pairs once and adds the j-side forces and potentials with float4 reductions.
+   * Automatic = 1: on B200 the cluster kernel evaluates 757 pair slots per atom (8x4 masks
+   * are 38 % full at r_list 1.1 nm) against 578 per-atom entries and is slower.
+   * Both give the same pair set (cph_get_pairlist, bit-exact) and agree to rounding;
+   * deterministic = 1 requires 0 or 1 (the j-side reductions of 2 are order-dependent,
+   * CPH_E_INVALID). */
+  int32_t pair_list;
 } cph_params;
 
 /* DBO event kinds (cph_dbo_event.kind) */

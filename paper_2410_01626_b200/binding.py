@@ -18,7 +18,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CPH_LIB", os.path.join(_HERE, "libcph.so"))   # CPH_LIB: A/B builds
 
-CPH_ABI_VERSION = 4
+CPH_ABI_VERSION = 5
 STATUS = {0: "CPH_OK", 1: "CPH_E_INVALID", 2: "CPH_E_CUDA", 3: "CPH_E_DIVERGED", 4: "CPH_E_STATE",
           5: "CPH_E_OOM", 6: "CPH_E_UNSUPPORTED"}
 ENERGY_TERMS = ("LJ", "real", "excl", "self", "recip", "net", "hi", "bias", "KE_atoms", "KE_lambda", "total")
@@ -59,7 +59,7 @@ class cph_params(C.Structure):
                 ("thermostat", C.c_int32), ("tau_atom", C.c_double), ("tau_lambda", C.c_double),
                 ("n_ph_levels", C.c_int32), ("ph_levels", _f64p), ("remd_first", C.c_int32),
                 ("remd_total", C.c_int32), ("hamiltonian", C.c_int32), ("deterministic", C.c_int32),
-                ("sub_batches", C.c_int32)]
+                ("sub_batches", C.c_int32), ("pair_list", C.c_int32)]
 
 
 class cph_dbo_event(C.Structure):
@@ -175,7 +175,7 @@ _FLOAT_PARAMS = ("dt", "temperature", "gamma_atom", "gamma_lambda", "lambda_mass
                  "dbo_barrier_step", "dbo_barrier_min", "dbo_barrier_max")
 _INT_PARAMS = ("pme_order", "nstlist", "nstout", "nstenergy", "frame_capacity", "dbo_well", "dbo_barrier",
                "dbo_well_steps", "dbo_barrier_steps", "dbo_censor_steps", "hamiltonian", "deterministic",
-               "sub_batches")
+               "sub_batches", "pair_list")
 KNOWN_PARAMS = frozenset(_FLOAT_PARAMS + _INT_PARAMS + ("thermostat", "pme_grid"))
 
 

@@ -30,7 +30,14 @@ constexpr int kMaxAtoms = 1 << 21;
 
 // Device-side flags (int array)
 enum { FLAG_PENDING_CLOSE = 0, FLAG_LIST_OVERFLOW = 1, FLAG_DIVERGED = 2, FLAG_MAX_NNB = 3,
-       FLAG_STEP_DONE = 4, FLAG_BAD_STATE = 5, FLAG_REMD_BAD = 6, FLAG_MOVED = 7, FLAG_COUNT = 8 };
+       FLAG_STEP_DONE = 4, FLAG_BAD_STATE = 5, FLAG_REMD_BAD = 6, FLAG_MOVED = 7,
+       FLAG_CL_OVERFLOW = 8, FLAG_CL_MAX = 9, FLAG_COUNT = 10 };
+
+// cluster pair-list entry word: j-cluster index J (slots 4J..4J+3) | image code << kEntryImgShift
+constexpr uint32_t kClJMask = 0x7FFFFu;
+constexpr int kClI = 8;                      // atoms per i-cluster
+constexpr int kClJ = 4;                      // atoms per j-cluster
+constexpr int kClSuper = 32;                 // atoms per super-cluster (4 i-clusters, one warp)
 
 // Scalars every kernel needs, passed by value.
 struct KParams {
@@ -48,7 +55,10 @@ struct KParams {
   int nb_packed;               // pair kernel: FFMA2 path for non-lambda warps (A/B: CPH_NB_PACKED=0)
   int det;                     // deterministic (fixed-point) PME spread
   // list
-  int cap;                     // neighbour capacity per atom
+  int cap;                     // neighbour capacity per atom (per-atom list; lambda-atom lists)
+  int pair_mode;               // 0 per-atom full list, 1 cluster-pair list (cph_params.pair_list)
+  int nsc;                     // super-cluster ids per replica (cluster mode): Nst/32 + columns + 1
+  int clcap;                   // entries per super-cluster (cluster mode)
   // PME
   int K[3], K3, Kc;            // grid, K^3, complex points per replica
   int Kzc;                     // Kz/2+1
@@ -89,6 +99,12 @@ struct DevBufs {
   int *cell_count = nullptr, *cell_start = nullptr; // [R*ncell], [R*(ncell+1)]
   int *perm_tmp = nullptr;                          // [R*Nst] new slot -> old slot
   uint32_t *nbl = nullptr;                          // [R*cap*Nst]
+  // cluster-pair list (pair_mode 1): per super-cluster id its first slot, atom count, entries
+  uint32_t *cl_j = nullptr;                         // [R*nsc*clcap] J | image code << 26
+  uint4 *cl_m = nullptr;                            // [R*nsc*clcap] interaction mask per i-cluster
+  int *cl_n = nullptr, *sc_first = nullptr, *sc_ni = nullptr;   // [R*nsc]
+  uint32_t *lam_nbl = nullptr;                      // [R*nlam*cap] full rows of the lambda atoms (slot | code << 26)
+  int *lam_n = nullptr;                             // [R*nlam]
   int *nnb = nullptr;                               // [R*Nst]
   int *excl_ptr = nullptr, *excl_idx = nullptr;     // CSR by original atom
   float2 *ljtab = nullptr;                          // [T*T] (6 c6, 12 c12) fp32
@@ -198,6 +214,7 @@ struct Ctx {
   int graph_block_kernels = 0;
   std::string err;
   size_t cap_grow = 0;
+  size_t clcap_grow = 0;
 };
 
 // ---- launchers (each returns the number of kernels it launched) ----------------------

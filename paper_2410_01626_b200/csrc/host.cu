@@ -384,6 +384,15 @@ cph_status check_flags(Ctx &c) {
              f[FLAG_MAX_NNB], c.kp.cap);
     c.err = buf;
     c.cap_grow = (size_t)f[FLAG_MAX_NNB];
+    if (f[FLAG_CL_OVERFLOW]) c.clcap_grow = (size_t)f[FLAG_CL_MAX];
+    return CPH_E_STATE;
+  }
+  if (f[FLAG_CL_OVERFLOW]) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "cluster pair list overflow: %d entries > capacity %d; results since the last rebuild are invalid",
+             f[FLAG_CL_MAX], c.kp.clcap);
+    c.err = buf;
+    c.clcap_grow = (size_t)f[FLAG_CL_MAX];
     return CPH_E_STATE;
   }
   return CPH_OK;
@@ -484,6 +493,7 @@ void cph_default_params(cph_params *p) {
   p->hamiltonian = 0;
   p->deterministic = 0;
   p->sub_batches = 0;
+  p->pair_list = 0;
 }
 
 
@@ -531,6 +541,8 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   if (prm->thermostat != 0 && prm->thermostat != 1) return bad("thermostat must be 0 (Langevin) or 1 (Bussi)");
   if (prm->hamiltonian != 0 && prm->hamiltonian != 1) return bad("hamiltonian must be 0 or 1");
   if (prm->deterministic != 0 && prm->deterministic != 1) return bad("deterministic must be 0 or 1");
+  if (prm->pair_list < 0 || prm->pair_list > 2) return bad("pair_list must be 0, 1 or 2");
+  if (prm->deterministic && prm->pair_list == 2) return bad("deterministic = 1 needs the per-atom pair list (pair_list 0 or 1)");
   if (prm->thermostat == 1 && !(prm->tau_atom > 0.0 && prm->tau_lambda > 0.0))
     return bad("Bussi coupling times must be > 0");
   std::vector<int> labels0;
@@ -678,10 +690,31 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   }
   kp.nb_packed = getenv("CPH_NB_PACKED") ? atoi(getenv("CPH_NB_PACKED")) : 1;
   kp.det = prm->deterministic;
+  // pair-list layout (cph_params.pair_list): automatic = the per-atom full list, which is the
+  // faster one on B200 (the cluster-pair kernel evaluates 757 pair slots per atom
+  // against 578 list entries and issues 1.7x the instructions); CPH_PAIR=atom|cluster overrides
+  // the automatic choice for A/B runs.  Deterministic mode needs the per-atom list (the cluster
+  // kernel's j-side float4 reductions are order-dependent).
+  kp.pair_mode = prm->pair_list == 2 ? 1 : 0;
+  if (prm->pair_list == 0 && getenv("CPH_PAIR")) kp.pair_mode = getenv("CPH_PAIR")[0] == 'c' ? 1 : 0;
+  if (kp.det) kp.pair_mode = 0;
   {
     const double expect = (double)N / V * 4.0 / 3.0 * kPi * std::pow(prm->rlist, 3);
     kp.cap = (int)std::ceil(1.6 * expect + 64.0);
     kp.cap = (kp.cap + 7) / 8 * 8;
+    // cluster mode: super-cluster ids and entry capacity.  Entries of a super-cluster ~ the
+    // j-clusters (4 atoms) within r_list of its region (one cell column wide, 32 atoms tall),
+    // half of them (each pair once): rho V / 8 with V the region dilated by r_list + 0.15 nm
+    // (the j-cluster extent), with a 2.5x margin (the mean is ~ 240 at density 100 nm^-3, dense solute regions reach ~1.8x)
+    int ncol = 1;
+    for (int d = 0; d < 2; ++d) ncol *= std::max(1, (int)std::floor(sys->box[d] / (0.5 * prm->rlist * (1.0 + 1e-4))));
+    kp.nsc = kp.Nst / kClSuper + ncol + 1;
+    const double rho = (double)N / V;
+    const double ca = std::sqrt(sys->box[0] * sys->box[1] / ncol), cz = kClSuper / (rho * ca * ca);
+    const double Rr = prm->rlist + 0.15;
+    const double Vm = ca * ca * cz + 2.0 * (ca * ca + 2.0 * ca * cz) * Rr + kPi * (2.0 * ca + cz) * Rr * Rr +
+                      4.0 / 3.0 * kPi * Rr * Rr * Rr;
+    kp.clcap = (int)std::ceil(2.5 * rho * Vm / 8.0 + 128.0);
   }
   for (int d = 0; d < 3; ++d) kp.K[d] = prm->pme_grid[d];
   kp.K3 = kp.K[0] * kp.K[1] * kp.K[2];
@@ -803,8 +836,23 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   d.cell_count = dalloc<int>(c, (size_t)R * kp.ncell);
   d.cell_start = dalloc<int>(c, (size_t)R * (kp.ncell + 1));
   d.perm_tmp = dalloc<int>(c, RN);
-  d.nbl = dalloc<uint32_t>(c, RN * kp.cap);
-  d.nnb = dalloc<int>(c, RN);
+  if (kp.pair_mode == 0) {
+    d.nbl = dalloc<uint32_t>(c, RN * kp.cap);
+    d.nnb = dalloc<int>(c, RN);
+  } else {
+    const size_t ns = (size_t)R * kp.nsc;
+    d.cl_j = dalloc<uint32_t>(c, ns * kp.clcap);
+    d.cl_m = dalloc<uint4>(c, ns * kp.clcap);
+    d.cl_n = dalloc<int>(c, ns);
+    d.sc_first = dalloc<int>(c, ns);
+    d.sc_ni = dalloc<int>(c, ns);
+    d.lam_nbl = dalloc<uint32_t>(c, std::max<size_t>(1, (size_t)R * nlam * kp.cap));
+    d.lam_n = dalloc<int>(c, std::max<size_t>(1, (size_t)R * nlam));
+    if (!d.cl_j || !d.cl_m || !d.cl_n || !d.sc_first || !d.sc_ni || !d.lam_nbl || !d.lam_n) {
+      c.err = "device allocation failed";
+      return fail_create(ctx, CPH_E_OOM);
+    }
+  }
   d.excl_ptr = dalloc<int>(c, N + 1);
   d.excl_idx = dalloc<int>(c, c.h_excl_idx.size());
   d.ljtab = dalloc<float2>(c, (size_t)T * T);
@@ -868,7 +916,7 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
     d.remd_acc = dalloc<long long>(c, (size_t)L * (P - 1));
     if (!d.remd_acc) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
   }
-  for (void *p : {(void *)d.xyzq, (void *)d.nbl, (void *)d.grid, (void *)d.cgrid, (void *)d.flags, (void *)d.seed})
+  for (void *p : {(void *)d.xyzq, kp.pair_mode ? (void *)d.cl_j : (void *)d.nbl, (void *)d.grid, (void *)d.cgrid, (void *)d.flags, (void *)d.seed})
     if (!p) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
   if (c.allocations.size() < 40) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
 
@@ -983,14 +1031,31 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   if (st == CPH_OK) st = check_flags(c);
   // a denser-than-average region overflowed the list capacity: grow it once (with margin)
   // and rebuild; an overflow during stepping is reported by the next call instead
-  if (st == CPH_E_STATE && c.cap_grow > (size_t)kp.cap) {
-    const int newcap = (int)((c.cap_grow * 5 / 4 + 64 + 7) / 8 * 8);
-    void *old = c.d.nbl;
-    c.allocations.erase(std::remove(c.allocations.begin(), c.allocations.end(), old), c.allocations.end());
-    if (c.dev_free) c.dev_free(old, c.alloc_ctx); else cudaFree(old);
-    kp.cap = newcap;
-    d.nbl = dalloc<uint32_t>(c, RN * kp.cap);
-    if (!d.nbl) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
+  if (st == CPH_E_STATE && (c.cap_grow > (size_t)kp.cap || c.clcap_grow > (size_t)kp.clcap)) {
+    auto release = [&](void *old) {
+      c.allocations.erase(std::remove(c.allocations.begin(), c.allocations.end(), old), c.allocations.end());
+      if (c.dev_free) c.dev_free(old, c.alloc_ctx); else cudaFree(old);
+    };
+    if (c.cap_grow > (size_t)kp.cap) {
+      kp.cap = (int)((c.cap_grow * 5 / 4 + 64 + 7) / 8 * 8);
+      if (kp.pair_mode == 0) {
+        release(d.nbl);
+        d.nbl = dalloc<uint32_t>(c, RN * kp.cap);
+        if (!d.nbl) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
+      } else {
+        release(d.lam_nbl);
+        d.lam_nbl = dalloc<uint32_t>(c, std::max<size_t>(1, (size_t)R * nlam * kp.cap));
+        if (!d.lam_nbl) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
+      }
+    }
+    if (c.clcap_grow > (size_t)kp.clcap) {
+      kp.clcap = (int)(c.clcap_grow * 5 / 4 + 64);
+      release(d.cl_j);
+      release(d.cl_m);
+      d.cl_j = dalloc<uint32_t>(c, (size_t)R * kp.nsc * kp.clcap);
+      d.cl_m = dalloc<uint4>(c, (size_t)R * kp.nsc * kp.clcap);
+      if (!d.cl_j || !d.cl_m) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
+    }
     const int zero[FLAG_COUNT] = {0};
     if (cudaMemcpy(d.flags, zero, sizeof(zero), cudaMemcpyHostToDevice) != cudaSuccess) {
       c.err = "flag reset failed";
@@ -1494,18 +1559,54 @@ struct ListHost {
   std::vector<int2> meta;
   std::vector<int> iperm;
   std::vector<uint32_t> nbl;
+  std::vector<int64_t> rp;       // cluster mode: directed partner slots of every slot (CSR)
+  std::vector<int> cols;
 };
 
 static cph_status fetch_list(Ctx &c, int r, ListHost &h) {
   const KParams &kp = c.kp;
   const size_t N = kp.N, base = (size_t)r * kp.Nst;
-  h.nnb.resize(N);
   h.meta.resize(N);
   h.iperm.resize(N);
-  h.nbl.resize((size_t)kp.cap * kp.Nst);
-  CK(cudaMemcpy(h.nnb.data(), c.d.nnb + base, sizeof(int) * N, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(h.meta.data(), c.d.meta + base, sizeof(int2) * N, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(h.iperm.data(), c.d.iperm + (size_t)r * N, sizeof(int) * N, cudaMemcpyDeviceToHost));
+  if (kp.pair_mode == 1) {
+    // every set mask bit of every entry is one pair the kernel evaluates, acting on both atoms
+    const size_t ns = kp.nsc, sb = (size_t)r * ns;
+    std::vector<int> n(ns), first(ns), ni(ns);
+    std::vector<uint32_t> cj(ns * kp.clcap);
+    std::vector<uint4> cm(ns * kp.clcap);
+    CK(cudaMemcpy(n.data(), c.d.cl_n + sb, sizeof(int) * ns, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(first.data(), c.d.sc_first + sb, sizeof(int) * ns, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ni.data(), c.d.sc_ni + sb, sizeof(int) * ns, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cj.data(), c.d.cl_j + sb * kp.clcap, sizeof(uint32_t) * cj.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cm.data(), c.d.cl_m + sb * kp.clcap, sizeof(uint4) * cm.size(), cudaMemcpyDeviceToHost));
+    std::vector<int> pi, pj;
+    for (size_t id = 0; id < ns; ++id) {
+      if (!ni[id]) continue;
+      for (int e = 0; e < std::min(n[id], kp.clcap); ++e) {
+        const size_t k = id * kp.clcap + e;
+        const uint32_t w[4] = {cm[k].x, cm[k].y, cm[k].z, cm[k].w};
+        const int J = (int)(cj[k] & kClJMask);
+        for (int s = 0; s < 4; ++s)
+          for (int bit = 0; bit < 32; ++bit)
+            if ((w[s] >> bit) & 1u) {
+              pi.push_back(first[id] + 8 * s + (bit & 7));
+              pj.push_back(4 * J + (bit >> 3));
+            }
+      }
+    }
+    h.rp.assign(N + 1, 0);
+    for (size_t k = 0; k < pi.size(); ++k) { ++h.rp[pi[k] + 1]; ++h.rp[pj[k] + 1]; }
+    for (size_t k = 0; k < N; ++k) h.rp[k + 1] += h.rp[k];
+    h.cols.resize(h.rp[N]);
+    std::vector<int64_t> fill(h.rp.begin(), h.rp.end() - 1);
+    for (size_t k = 0; k < pi.size(); ++k) { h.cols[fill[pi[k]]++] = pj[k]; h.cols[fill[pj[k]]++] = pi[k]; }
+    return CPH_OK;
+  }
+  h.nnb.resize(N);
+  h.nbl.resize((size_t)kp.cap * kp.Nst);
+  CK(cudaMemcpy(h.nnb.data(), c.d.nnb + base, sizeof(int) * N, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(h.nbl.data(), c.d.nbl + (size_t)r * kp.cap * kp.Nst, sizeof(uint32_t) * h.nbl.size(),
                 cudaMemcpyDeviceToHost));
   return CPH_OK;
@@ -1514,6 +1615,10 @@ static cph_status fetch_list(Ctx &c, int r, ListHost &h) {
 template <class F>
 static void list_row(const Ctx &c, const ListHost &h, int slot, F emit) {
   const KParams &kp = c.kp;
+  if (kp.pair_mode == 1) {
+    for (int64_t k = h.rp[slot]; k < h.rp[slot + 1]; ++k) emit(h.meta[h.cols[k]].x);
+    return;
+  }
   for (int k = 0; k < std::min(h.nnb[slot], kp.cap); ++k) {
     const int j = (int)(h.nbl[((size_t)(k / 8) * kp.Nst + slot) * 8 + (k % 8)] & kEntryJMask);
     if (j != slot) emit(h.meta[j].x);

@@ -651,6 +651,256 @@ __global__ void __launch_bounds__(32 * kColWarps) k_build_list_col(KParams kp, D
   }
 }
 
+// ---- cluster-pair list (cph_params.pair_list = 2) ------------------------------
+// Super-clusters are 32 consecutive atoms of one cell column (column-aligned; the last one of a
+// column is partial); super-cluster id = floor(column start / 32) + column index + k, unique
+// because column c holds ceil(n_c / 32) <= n_c / 32 + 1 of them.  i-cluster s of a super-cluster
+// = its atoms 8s .. 8s+7; j-clusters are globally aligned groups of 4 sorted slots.  For every
+// canonical pair (i, j) (R14, not excluded) with slot_i < slot_j, the super-cluster of
+// i holds an entry (J = slot_j / 4, image code) whose mask word s has bit (slot_j % 4) * 8 + a,
+// a = (slot_i - first) % 8: the bits are exactly the canonical half list.  One warp per
+// super-cluster walks the 25 stencil columns like the column builder (union z window of its
+// atoms, home and z-image runs), restricted to slots > its first atom, stages 32 slots at a time
+// (4-aligned, so a group of 4 staged candidates is one j-cluster) and takes the four per-lane
+// decisions of a group with the same fast d^2 / rounding-band / exact canonical test as the
+// column builder; four ballots give the group's masks and lane 0 appends the entry.
+constexpr int kClWarps = 8;
+
+__global__ void __launch_bounds__(32 * kClWarps, 2) k_build_cluster(KParams kp, DevBufs d) {
+  const int r = blockIdx.y, colid = blockIdx.x;
+  const int cx = colid / kp.nc[1], cy = colid % kp.nc[1];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t base = (size_t)r * kp.Nst;
+  const float4 *xq = d.xyzq + base;
+  const int2 *meta = d.meta + base;
+  const int *start = d.cell_start + (size_t)r * (kp.ncell + 1);
+  const int nz = kp.nc[2];
+  const int cb = start[colid * nz], ce = start[colid * nz + nz];
+  const float3 Lbox = make_float3(kp.L[0], kp.L[1], kp.L[2]);
+  const float3 Linv = make_float3(kp.invL[0], kp.invL[1], kp.invL[2]);
+  const float rlist2 = kp.rlist2;
+  const float lo2 = kp.rlist2 * (1.0f - 3e-5f), hi2 = kp.rlist2 * (1.0f + 3e-5f);
+  const float2 nmid = make_float2(-0.5f * (lo2 + hi2), -0.5f * (lo2 + hi2));
+  const float hw = 0.5f * (hi2 - lo2) * 1.01f;
+  const float csx = kp.L[0] / (float)kp.nc[0], csy = kp.L[1] / (float)kp.nc[1], csz = kp.L[2] / (float)nz;
+  const float win_r = sqrtf(kp.rlist2) * 1.0001f + kWinPad;
+  const float win_r2 = win_r * win_r;
+  __shared__ int s_colc[25], s_code[25];
+  __shared__ float s_sx[25], s_sy[25], s_xlo[25], s_ylo[25];
+  __shared__ __align__(16) float s_px[kClWarps][32], s_py[kClWarps][32], s_pz[kClWarps][32];
+  __shared__ int s_org[kClWarps][32];
+  if (threadIdx.x < 25) {
+    const int k = c_walk[threadIdx.x * 5] / 5;
+    const int rx = cx - 2 + k / 5, ry = cy - 2 + k % 5;
+    const int wx = (rx + 2 * kp.nc[0]) / kp.nc[0] - 2, wy = (ry + 2 * kp.nc[1]) / kp.nc[1] - 2;
+    s_colc[threadIdx.x] = ((rx - wx * kp.nc[0]) * kp.nc[1] + (ry - wy * kp.nc[1])) * nz;
+    s_sx[threadIdx.x] = kp.L[0] * (float)wx;
+    s_sy[threadIdx.x] = kp.L[1] * (float)wy;
+    s_xlo[threadIdx.x] = (float)rx * csx - kWinPad;
+    s_ylo[threadIdx.x] = (float)ry * csy - kWinPad;
+    s_code[threadIdx.x] = (1 - wx) * 9 + (1 - wy) * 3;
+  }
+  __syncthreads();
+  float *px = s_px[w], *py = s_py[w], *pz = s_pz[w];
+  int *so = s_org[w];
+  const int sc0 = cb / kClSuper + colid;
+  for (int k = w; kClSuper * k < ce - cb; k += kClWarps) {
+    const int first = cb + kClSuper * k, ni = min(kClSuper, ce - first);
+    const size_t sidx = (size_t)r * kp.nsc + sc0 + k;
+    const int i = first + lane;
+    const bool valid = lane < ni;
+    const float4 xi = valid ? xq[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int orig = valid ? meta[i].x : 0;
+    const int eb = valid ? d.excl_ptr[orig] : 0, ee = valid ? d.excl_ptr[orig + 1] : 0;
+    const bool warp_excl = __any_sync(0xffffffffu, ee > eb);
+    const float2 nxi = make_float2(-xi.x, -xi.x), nyi = make_float2(-xi.y, -xi.y), nzi = make_float2(-xi.z, -xi.z);
+    uint32_t *oj = d.cl_j + sidx * kp.clcap;
+    uint4 *om = d.cl_m + sidx * kp.clcap;
+    int cnt = 0;
+    auto excluded = [&](int o) {
+      bool ex = false;
+      for (int e = eb; e < ee; ++e) ex |= (d.excl_idx[e] == o);
+      return ex;
+    };
+    for (int q = 0; q < 25; ++q) {
+      const float xlo = s_xlo[q], ylo = s_ylo[q];
+      const float ddx = fmaxf(0.f, fmaxf(xlo - xi.x, xi.x - (xlo + csx + 2.f * kWinPad)));
+      const float ddy = fmaxf(0.f, fmaxf(ylo - xi.y, xi.y - (ylo + csy + 2.f * kWinPad)));
+      const float rr2 = win_r2 - ddx * ddx - ddy * ddy;
+      float zlo = INFINITY, zhi = -INFINITY;
+      if (valid && rr2 > 0.f) {
+        const float rr = sqrtf(rr2);
+        zlo = xi.z - rr;
+        zhi = xi.z + rr;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        zlo = fminf(zlo, __shfl_xor_sync(0xffffffffu, zlo, o));
+        zhi = fmaxf(zhi, __shfl_xor_sync(0xffffffffu, zhi, o));
+      }
+      if (!(zlo <= zhi)) continue;
+      const int colc = s_colc[q];
+      const float wsx = s_sx[q], wsy = s_sy[q];
+      for (int part = 0; part < 3; ++part) {
+        float a, b, wsz;
+        int wz;
+        if (part == 0) { a = fmaxf(zlo, 0.f); b = fminf(zhi, kp.L[2]); wsz = 0.f; wz = 0; }
+        else if (part == 1) {
+          if (!(zlo < 0.f)) continue;
+          a = zlo + kp.L[2]; b = kp.L[2]; wsz = -kp.L[2]; wz = -1;
+        } else {
+          if (!(zhi > kp.L[2])) continue;
+          a = 0.f; b = zhi - kp.L[2]; wsz = kp.L[2]; wz = 1;
+        }
+        if (!(a <= b)) continue;
+        const int c0 = max(0, min((int)floorf(a / csz), nz - 1));
+        const int c1 = max(0, min((int)floorf(b / csz), nz - 1));
+        const int j0 = max(start[colc + c0], first + 1), j1 = start[colc + c1 + 1];   // half list: j > first
+        if (j0 >= j1) continue;
+        const uint32_t code = (uint32_t)(s_code[q] + (1 - wz));
+        const float zwlo = zlo - wsz, zwhi = zhi - wsz;
+        for (int jb = j0 & ~3; jb < j1; jb += 32) {
+          const int js = jb + lane;
+          const bool in = js >= j0 && js < j1;
+          __syncwarp();
+          float zt = 0.f;
+          if (in) {
+            const float4 p = xq[js];
+            px[lane] = p.x + wsx;
+            py[lane] = p.y + wsy;
+            pz[lane] = p.z + wsz;
+            so[lane] = meta[js].x;
+            zt = p.z;
+          } else {
+            px[lane] = py[lane] = pz[lane] = 1e30f;
+            so[lane] = -1;
+          }
+          // the run [j0, j1) is z-sorted: the union window is a contiguous slice of it
+          const int lo_l = max(0, j0 - jb);
+          const int tb = lo_l + __popc(__ballot_sync(0xffffffffu, in && zt < zwlo));
+          const int te = lo_l + __popc(__ballot_sync(0xffffffffu, in && zt <= zwhi));
+          __syncwarp();
+          for (int t0 = tb & ~3; t0 < te; t0 += 4) {
+            const float4 x4 = *reinterpret_cast<const float4 *>(px + t0);
+            const float4 y4 = *reinterpret_cast<const float4 *>(py + t0);
+            const float4 z4 = *reinterpret_cast<const float4 *>(pz + t0);
+            const float2 dxa = __fadd2_rn(make_float2(x4.x, x4.y), nxi), dxb = __fadd2_rn(make_float2(x4.z, x4.w), nxi);
+            const float2 dya = __fadd2_rn(make_float2(y4.x, y4.y), nyi), dyb = __fadd2_rn(make_float2(y4.z, y4.w), nyi);
+            const float2 dza = __fadd2_rn(make_float2(z4.x, z4.y), nzi), dzb = __fadd2_rn(make_float2(z4.z, z4.w), nzi);
+            const float2 qa = __ffma2_rn(dxa, dxa, __ffma2_rn(dya, dya, __fmul2_rn(dza, dza)));
+            const float2 qb = __ffma2_rn(dxb, dxb, __ffma2_rn(dyb, dyb, __fmul2_rn(dzb, dzb)));
+            const float2 ma = __fadd2_rn(qa, nmid), mb = __fadd2_rn(qb, nmid);
+            const float d2[4] = {qa.x, qa.y, qb.x, qb.y};
+            const int jt = jb + t0;                               // slot of candidate u = jt + u
+            bool acc[4];
+            if (!__any_sync(0xffffffffu, fminf(fminf(fabsf(ma.x), fabsf(ma.y)), fminf(fabsf(mb.x), fabsf(mb.y))) <= hw)) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) acc[u] = valid && d2[u] < lo2 && jt + u > i;
+            } else {                                              // rare: a candidate near r_list^2
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                bool ok = valid && d2[u] < hi2 && jt + u > i;
+                if (ok && !(d2[u] < lo2)) {
+                  int cc;
+                  ok = canonical_in_code(xq[jt + u], xi, Lbox, Linv, rlist2, &cc) && cc == (int)code;
+                }
+                acc[u] = ok;
+              }
+            }
+            if (warp_excl) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (acc[u] && ee > eb) acc[u] = !excluded(so[t0 + u]);
+            }
+            const uint32_t B0 = __ballot_sync(0xffffffffu, acc[0]), B1 = __ballot_sync(0xffffffffu, acc[1]);
+            const uint32_t B2 = __ballot_sync(0xffffffffu, acc[2]), B3 = __ballot_sync(0xffffffffu, acc[3]);
+            if ((B0 | B1 | B2 | B3) == 0u) continue;
+            if (lane == 0) {
+              // ballot bit l = 8 s + a  ->  mask word s, bit u * 8 + a
+              uint32_t m[4];
+#pragma unroll
+              for (int s = 0; s < 4; ++s)
+                m[s] = ((B0 >> (8 * s)) & 0xFFu) | (((B1 >> (8 * s)) & 0xFFu) << 8) | (((B2 >> (8 * s)) & 0xFFu) << 16) |
+                       (((B3 >> (8 * s)) & 0xFFu) << 24);
+              if (cnt < kp.clcap) {
+                oj[cnt] = (uint32_t)(jt >> 2) | (code << kEntryImgShift);
+                om[cnt] = make_uint4(m[0], m[1], m[2], m[3]);
+              }
+            }
+            ++cnt;
+          }
+        }
+      }
+    }
+    if (lane == 0) {
+      d.cl_n[sidx] = cnt;
+      d.sc_first[sidx] = first;
+      d.sc_ni[sidx] = ni;
+      if (cnt > kp.clcap) {
+        d.flags[FLAG_CL_OVERFLOW] = 1;
+        atomicMax(&d.flags[FLAG_CL_MAX], cnt);
+      }
+    }
+  }
+}
+
+// Full canonical rows of the lambda atoms (both directions, slot order per stencil cell) for the
+// fp64 real-space potential of the lambda atoms in cluster mode (k_phi_lam): one warp per lambda
+// atom, every cell of its 5x5x5 stencil (whole dimensions below 5 cells) visited once, the exact
+// canonical decision with the pair's own image code, ballot-compacted in-order appends.
+__global__ void __launch_bounds__(32) k_build_lam_list(KParams kp, DevBufs d) {
+  const int r = blockIdx.y, k = blockIdx.x, lane = threadIdx.x;
+  const size_t base = (size_t)r * kp.Nst;
+  const float4 *xq = d.xyzq + base;
+  const int2 *meta = d.meta + base;
+  const int *start = d.cell_start + (size_t)r * (kp.ncell + 1);
+  const int orig = d.g_atoms[k];
+  const int i = d.iperm[(size_t)r * kp.N + orig];
+  const float4 xi = xq[i];
+  const float3 Lbox = make_float3(kp.L[0], kp.L[1], kp.L[2]);
+  const float3 Linv = make_float3(kp.invL[0], kp.invL[1], kp.invL[2]);
+  const int eb = d.excl_ptr[orig], ee = d.excl_ptr[orig + 1];
+  int ci[3];
+  {
+    const float p[3] = {xi.x, xi.y, xi.z};
+    for (int dd = 0; dd < 3; ++dd) ci[dd] = cell_coord(p[dd], kp.invL[dd], kp.nc[dd]);
+  }
+  uint32_t *out = d.lam_nbl + ((size_t)r * kp.nlam + k) * kp.cap;
+  int cnt = 0;
+  for (int ox = 0; ox < kp.ns[0]; ++ox)
+    for (int oy = 0; oy < kp.ns[1]; ++oy)
+      for (int oz = 0; oz < kp.ns[2]; ++oz) {
+        const int gx = kp.ns[0] == 5 ? (ci[0] - 2 + ox + kp.nc[0]) % kp.nc[0] : ox;
+        const int gy = kp.ns[1] == 5 ? (ci[1] - 2 + oy + kp.nc[1]) % kp.nc[1] : oy;
+        const int gz = kp.ns[2] == 5 ? (ci[2] - 2 + oz + kp.nc[2]) % kp.nc[2] : oz;
+        const int cc = (gx * kp.nc[1] + gy) * kp.nc[2] + gz;
+        const int jb = start[cc], je = start[cc + 1];
+        for (int j0 = jb; j0 < je; j0 += 32) {
+          const int j = j0 + lane;
+          bool ok = false;
+          int code = 13;
+          if (j < je && j != i) {
+            ok = canonical_in_code(xq[j], xi, Lbox, Linv, kp.rlist2, &code);
+            if (ok && ee > eb) {
+              const int o = meta[j].x;
+              for (int e = eb; e < ee; ++e) ok &= (d.excl_idx[e] != o);
+            }
+          }
+          const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+          const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
+          if (ok && pos < kp.cap) out[pos] = (uint32_t)j | ((uint32_t)code << kEntryImgShift);
+          cnt += __popc(bal);
+        }
+      }
+  if (lane == 0) {
+    d.lam_n[(size_t)r * kp.nlam + k] = cnt;
+    if (cnt > kp.cap) {
+      d.flags[FLAG_LIST_OVERFLOW] = 1;
+      atomicMax(&d.flags[FLAG_MAX_NNB], cnt);
+    }
+  }
+}
+
 // spatial sort + permutation of every per-atom array (positions wrapped); the pair list
 // itself is launch_build_list, so work that only needs the new atom order (the PME chain) can
 // start while the list is built
@@ -668,6 +918,14 @@ int launch_sort(Ctx &c, cudaStream_t s) {
 }
 
 int launch_build_list(Ctx &c, cudaStream_t s) {
+  if (c.kp.pair_mode == 1) {
+    const size_t n = (size_t)c.kp.R * c.kp.nsc;
+    cudaMemsetAsync(c.d.sc_ni, 0, sizeof(int) * n, s);
+    cudaMemsetAsync(c.d.cl_n, 0, sizeof(int) * n, s);
+    k_build_cluster<<<dim3(c.kp.nc[0] * c.kp.nc[1], c.kp.R), 32 * kClWarps, 0, s>>>(c.kp, c.d);
+    if (c.kp.nlam) k_build_lam_list<<<dim3(c.kp.nlam, c.kp.R), 32, 0, s>>>(c.kp, c.d);
+    return c.kp.nlam ? 2 : 1;
+  }
   static const bool by_cell = getenv("CPH_BUILD") && getenv("CPH_BUILD")[0] == 'c';   // A/B: one warp per cell
   if (by_cell) k_build_list<<<dim3(c.kp.ncell, c.kp.R), 32, 0, s>>>(c.kp, c.d);
   else k_build_list_col<<<dim3(c.kp.nc[0] * c.kp.nc[1], c.kp.R), 32 * kColWarps, 0, s>>>(c.kp, c.d);

@@ -75,7 +75,7 @@ def test_dbo_defaults_are_the_papers(cph):
     import ctypes
     p = cph.binding.cph_params()
     cph.lib().cph_default_params(ctypes.byref(p))
-    assert p.abi_version == 4 and p.deterministic == 0 and p.sub_batches == 0 and p.dbo_well == 0 and p.dbo_barrier == 0
+    assert p.abi_version == 5 and p.deterministic == 0 and p.sub_batches == 0 and p.pair_list == 0 and p.dbo_well == 0 and p.dbo_barrier == 0
     assert (p.dbo_well_steps, p.dbo_barrier_steps, p.dbo_censor_steps) == (20000, 500000, 5000)   # 40 ps, 1 ns, 10 ps
     assert (p.dbo_well_near, p.dbo_residency, p.dbo_well_tol, p.dbo_well_gain, p.dbo_well_cap) == (0.2, 0.7, 0.03, 0.5, 0.08)
     assert (p.dbo_trans_lo, p.dbo_trans_hi, p.dbo_target, p.dbo_target_tol) == (0.2, 0.8, 0.25, 0.05)
