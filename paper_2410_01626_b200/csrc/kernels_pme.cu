@@ -5,6 +5,9 @@
 //   theta_0 = w^3/6, theta_1 = (-3w^3+3w^2+3w+1)/6, theta_2 = (3w^3-6w^2+4)/6, theta_3 = (1-w)^3/6.
 // The FFTs are cuFFT plans (reported as their own line item).
 #include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdlib>
 
 #include "cph_device.cuh"
 
@@ -210,6 +213,155 @@ __global__ void __launch_bounds__(128) k_gather(KParams kp, DevBufs d) {
                                                 sc * gz * (float)kp.K[2] * kp.invL[2], phi);
 }
 
+// Brick-staged force gather (A/B alternative, CPH_GATHER=brick; the default is k_gather: at
+// C4 x 21 this kernel takes 0.070 ms per step against 0.057, at C5 x 8 0.134 against 0.142 --
+// a cell column's brick is ~2.4x its atoms' own xy footprint (3-point halo around 5.5 points),
+// so the staged bytes are ~33 floats per atom against 64 L1-hitting reads, and every chunk
+// waits for its copies).  One CTA of
+// kGbAtoms threads per cell column walks the column's z-sorted atoms kGbAtoms at a time; for
+// each chunk the grid region its 4x4x4 stencils cover (the chunk's base-index range per
+// dimension + 3, z rounded out to 16-byte blocks) is copied into shared memory with 1-D bulk
+// copies (cp.async.bulk, one or two per z row, completion counted on an mbarrier), then every
+// atom reads its 64 points from shared memory.  Same arithmetic and order as k_gather (equal to
+// rounding: the compiler contracts the two instantiations differently); an atom whose stencil is not inside the brick (it drifted far since
+// the rebuild, or the chunk's region exceeds the buffer) reads the global grid instead.
+#ifndef CPH_GB_ATOMS
+#define CPH_GB_ATOMS 128
+#endif
+constexpr int kGbAtoms = CPH_GB_ATOMS;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+template <class F>
+__device__ __forceinline__ float4 gather_atom(const KParams &kp, float4 p, int kx, int ky, int kz, const float tx[4],
+                                              const float ty[4], const float tz[4], const float dx[4], const float dy[4],
+                                              const float dz[4], F val) {
+  float phi = 0.f, gx = 0.f, gy = 0.f, gz = 0.f;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      float s = 0.f, sd = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float v = val(a, b, c);
+        s = fmaf(tz[c], v, s);
+        sd = fmaf(dz[c], v, sd);
+      }
+      phi = fmaf(tx[a] * ty[b], s, phi);
+      gx = fmaf(dx[a] * ty[b], s, gx);
+      gy = fmaf(tx[a] * dy[b], s, gy);
+      gz = fmaf(tx[a] * ty[b], sd, gz);
+    }
+  }
+  const float sc = -kp.fcoul * p.w;
+  return make_float4(sc * gx * (float)kp.K[0] * kp.invL[0], sc * gy * (float)kp.K[1] * kp.invL[1],
+                     sc * gz * (float)kp.K[2] * kp.invL[2], phi);
+}
+
+// signed offset of a base index from a reference, in [-K/2, K/2)
+__device__ __forceinline__ int wrap_off(int k, int ref, int K) { return ((k - ref + K + K / 2) % K) - K / 2; }
+
+__global__ void __launch_bounds__(kGbAtoms) k_gather_brick(KParams kp, DevBufs d, int cap) {
+  extern __shared__ __align__(128) float brick[];
+  __shared__ __align__(8) unsigned long long bar;
+  __shared__ int s_ext[6];
+  const int r = blockIdx.y, col = blockIdx.x, t = threadIdx.x;
+  const int nz = kp.nc[2];
+  const int *start = d.cell_start + (size_t)r * (kp.ncell + 1);
+  const int cs = start[col * nz], ce = start[col * nz + nz];
+  const int Kx = kp.K[0], Ky = kp.K[1], Kz = kp.K[2];
+  const float *g = d.grid + (size_t)r * kp.K3;
+  const float4 *xq = d.xyzq + (size_t)r * kp.Nst;
+  float4 *out = d.f_rec + (size_t)r * kp.Nst;
+  const int cxi = col / kp.nc[1], cyi = col % kp.nc[1];
+  const int refx = (int)(((float)cxi + 0.5f) * (float)Kx / (float)kp.nc[0]) % Kx;
+  const int refy = (int)(((float)cyi + 0.5f) * (float)Ky / (float)kp.nc[1]) % Ky;
+  if (t == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int c0 = cs; c0 < ce; c0 += kGbAtoms) {
+    const int i = c0 + t;
+    const bool valid = i < ce;
+    const float4 p = valid ? xq[i] : xq[c0];
+    int kx, ky, kz;
+    float tx[4], ty[4], tz[4], dx[4], dy[4], dz[4];
+    bspline4(p.x, kp.invL[0], Kx, kx, tx, dx);
+    bspline4(p.y, kp.invL[1], Ky, ky, ty, dy);
+    bspline4(p.z, kp.invL[2], Kz, kz, tz, dz);
+    // the chunk's base-index extents (x, y about the column centre, z about the first atom)
+    if (t < 6) s_ext[t] = (t & 1) ? INT_MIN : INT_MAX;
+    __syncthreads();
+    const int ox = wrap_off(kx, refx, Kx), oy = wrap_off(ky, refy, Ky);
+    int rz;
+    {
+      // one z reference for the whole CTA: the chunk's first atom
+      const float4 p0 = xq[c0];
+      const float tz0 = p0.z * kp.invL[2];
+      rz = (int)floorf((tz0 - floorf(tz0)) * (float)Kz);
+      if (rz >= Kz) rz -= Kz;
+    }
+    const int oz = wrap_off(kz, rz, Kz);
+    atomicMin(&s_ext[0], ox); atomicMax(&s_ext[1], ox);
+    atomicMin(&s_ext[2], oy); atomicMax(&s_ext[3], oy);
+    atomicMin(&s_ext[4], oz); atomicMax(&s_ext[5], oz);
+    __syncthreads();
+    const int x0 = refx + s_ext[0] - 3, BX = s_ext[1] - s_ext[0] + 4;
+    const int y0 = refy + s_ext[2] - 3, BY = s_ext[3] - s_ext[2] + 4;
+    const int zlo = rz + s_ext[4] - 3, zhi = rz + s_ext[5];                 // inclusive, unwrapped
+    const int z0 = zlo >= 0 ? (zlo & ~3) : -((-zlo + 3) & ~3);                // 16-byte aligned start
+    const int BZ = ((zhi + 1 - z0) + 3) & ~3;
+    const bool staged = BX * BY * BZ <= cap && BZ <= Kz && BX <= Kx && BY <= Ky;
+    if (staged) {
+      {
+        const int nrow = BX * BY;
+        const int zs = ((z0 % Kz) + Kz) % Kz;
+        const int n1 = min(BZ, Kz - zs), n2 = BZ - n1;                      // z run and its wrapped part
+        if (t == 0) {
+          const uint32_t bytes = (uint32_t)(nrow * BZ * 4);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(bytes) : "memory");
+        }
+        __syncthreads();                                   // expect_tx before any copy completes
+        for (int q = t; q < nrow; q += kGbAtoms) {
+          const int bx = q / BY, by = q % BY;
+          const int ix = ((x0 + bx) % Kx + Kx) % Kx, iy = ((y0 + by) % Ky + Ky) % Ky;
+          const float *src = g + ((size_t)ix * Ky + iy) * Kz;
+          float *dst = brick + (size_t)q * BZ;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           smem_u32(dst)), "l"(src + zs), "r"(n1 * 4), "r"(smem_u32(&bar)) : "memory");
+          if (n2 > 0)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             smem_u32(dst + n1)), "l"(src), "r"(n2 * 4), "r"(smem_u32(&bar)) : "memory");
+        }
+      }
+      // wait for the copies (phase parity)
+      asm volatile(
+          "{\n\t.reg .pred P1;\n\tLAB_WAIT%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+          "@!P1 bra.uni LAB_WAIT%=;\n\t}" ::"r"(smem_u32(&bar)), "r"(phase) : "memory");
+      phase ^= 1u;
+    }
+    if (valid) {
+      const int lx = ox - s_ext[0] + 3, ly = oy - s_ext[2] + 3, lz = (rz + oz) - z0;   // local base indices
+      float4 f;
+      if (staged && lx >= 3 && lx < BX && ly >= 3 && ly < BY && lz >= 3 && lz < BZ) {
+        f = gather_atom(kp, p, kx, ky, kz, tx, ty, tz, dx, dy, dz,
+                        [&](int a, int b, int c) { return brick[((lx - a) * BY + (ly - b)) * BZ + (lz - c)]; });
+      } else {
+        f = gather_atom(kp, p, kx, ky, kz, tx, ty, tz, dx, dy, dz, [&](int a, int b, int c) {
+          const int ix = (kx - a + Kx) % Kx, iy = (ky - b + Ky) % Ky, iz = (kz - c + Kz) % Kz;
+          return __ldg(g + ((size_t)ix * Ky + iy) * Kz + iz);
+        });
+      }
+      out[i] = f;
+    }
+    __syncthreads();   // the brick is rewritten by the next chunk's copies
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+}
+
 int launch_spread(Ctx &c, cudaStream_t s) {
   if (c.kp.det) {
     k_spread_fx<<<dim3((c.kp.N + 127) / 128, c.kp.R), 128, 0, s>>>(c.kp, c.d);
@@ -228,6 +380,17 @@ int launch_solve(Ctx &c, cudaStream_t s, int step_offset) {
   return 1;
 }
 int launch_gather(Ctx &c, cudaStream_t s) {
+  static const bool global = !(getenv("CPH_GATHER") && getenv("CPH_GATHER")[0] == 'b');   // A/B: brick gather
+  if (!global && c.kp.K[2] % 4 == 0) {   // 16-byte bulk copies need K_z % 4 == 0
+    // brick buffer: the x, y extent of a column (K / n_c + 3 points, plus drift) times the z
+    // extent of kGbAtoms atoms at the mean density, with margin; chunks that need more fall back
+    const double rho = (double)c.kp.N / ((double)c.kp.Ld[0] * c.kp.Ld[1] * c.kp.Ld[2]);
+    const double bx = std::ceil((double)c.kp.K[0] / c.kp.nc[0]) + 5.0, by = std::ceil((double)c.kp.K[1] / c.kp.nc[1]) + 5.0;
+    const double zext = kGbAtoms / (rho * (c.kp.Ld[0] / c.kp.nc[0]) * (c.kp.Ld[1] / c.kp.nc[1])) * c.kp.K[2] / c.kp.Ld[2];
+    const int cap = (int)std::min(bx * by * (std::ceil(1.5 * zext) + 12.0), 40.0 * 1024 / 4);   // <= 40 KB (static default)
+    k_gather_brick<<<dim3(c.kp.nc[0] * c.kp.nc[1], c.kp.R), kGbAtoms, cap * sizeof(float), s>>>(c.kp, c.d, cap);
+    return 1;
+  }
   dim3 grid((c.kp.N + 127) / 128, c.kp.R);
   k_gather<<<grid, 128, 0, s>>>(c.kp, c.d);
   return 1;
