@@ -302,7 +302,11 @@ def main():
     stream = torch.cuda.Stream(device=local)
     torch.cuda.set_stream(stream)
     ctx = cph.cph_create(s, pH, seeds, vel_replicas=vel, device=local, cuda_stream=stream.cuda_stream)
-    W = max(args.warmup, 3)
+    # untimed warm-up, rounded up to a whole number of pair-list blocks (nstlist steps, one CUDA
+    # graph each): the K timed steps then start on a block boundary and replay the captured
+    # graphs instead of launching the partial blocks kernel by kernel; "warmup" reports W as run
+    nst = int(s.params["nstlist"])
+    W = -(-max(args.warmup, 3) // nst) * nst
     K = args.steps
     ctx.cph_step(W)
     ctx.cph_sync()

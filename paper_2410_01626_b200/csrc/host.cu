@@ -1065,6 +1065,9 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
     st = evaluate_here(c, true);
     if (st == CPH_OK) st = check_flags(c);
   }
+  // the nstlist-block graph is captured now (capture records, runs nothing), so the first
+  // full block of a cph_step call replays it instead of paying capture + instantiation
+  if (st == CPH_OK) st = capture_block(c);
   if (st != CPH_OK) {
     cph_status s2 = st;
     if (c.plan_r2c) cufftDestroy(c.plan_r2c);
