@@ -387,7 +387,9 @@ cph_status cph_set_state(cph_ctx *ctx, int32_t replica, const void *buf, int64_t
  * cph_set_state_all re-evaluates forces once for the whole batch.  A restore re-sorts the atoms
  * and rebuilds the pair list unless every restored atom is where the last rebuild put it
  * (minimum-image displacement <= 1e-5 nm): then that list is the list of the restored
- * configuration and is kept. */
+ * configuration and is kept.  Headers and finiteness are checked before anything is
+ * overwritten (CPH_E_INVALID, state unchanged); the re-evaluation is enqueued on the context
+ * stream and not awaited, so a device-side failure in it is reported by the next call. */
 cph_status cph_get_state_all(cph_ctx *ctx, void *buf, int64_t cap, int64_t *n);
 cph_status cph_set_state_all(cph_ctx *ctx, const void *buf, int64_t n);
 

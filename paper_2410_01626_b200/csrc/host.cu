@@ -349,15 +349,26 @@ cph_status evaluate_here(Ctx &c, bool rebuild) {
   int k = 1;
   k += launch_set_charges(c, s);
   if (rebuild) k += launch_rebuild(c, s);
-  cufftSetStream(c.plan_r2c, s);
-  cufftSetStream(c.plan_c2r, s);
-  k += launch_spread(c, s);
+  // the PME chain on its own stream beside the pair kernel, joined before the lambda kernel
+  // (as in a step; CPH_ONE_STREAM serialises both, a diagnostic)
+  static const bool one = getenv("CPH_ONE_STREAM") != nullptr;
+  cudaStream_t sp = s;
+  if (!one) {
+    CK(cudaEventRecord(c.ev_fork, s));
+    CK(cudaStreamWaitEvent(c.stream_pme, c.ev_fork, 0));
+    sp = c.stream_pme;
+  }
+  cufftSetStream(c.plan_r2c, sp);
+  cufftSetStream(c.plan_c2r, sp);
+  k += launch_spread(c, sp);
   CKF(cufftExecR2C(c.plan_r2c, c.d.grid, (cufftComplex *)c.d.cgrid));
-  k += launch_solve(c, s, 0);
+  k += launch_solve(c, sp, 0);
   CKF(cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid));
-  k += launch_gather(c, s);
+  k += launch_gather(c, sp);
+  k += launch_hi_recip(c, sp);
+  if (!one) CK(cudaEventRecord(c.ev_join, sp));
   k += launch_nonbonded(c, s, 0);
-  k += launch_hi_recip(c, s);
+  if (!one) CK(cudaStreamWaitEvent(s, c.ev_join, 0));
   k += launch_hi_finish(c, s, 0);
   k += launch_lambda_reduce(c, s, 0);
   k += launch_close(c, s, 0);
@@ -856,6 +867,7 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   d.excl_ptr = dalloc<int>(c, N + 1);
   d.excl_idx = dalloc<int>(c, c.h_excl_idx.size());
   d.ljtab = dalloc<float2>(c, (size_t)T * T);
+  d.ljtab64 = dalloc<double2>(c, (size_t)T * T);
   d.phi64_nb = dalloc<double>(c, (size_t)R * nlam);
   d.phi_lam = dalloc<double>(c, (size_t)R * nlam);
   d.grid = dalloc<float>(c, (size_t)R * kp.K3);
@@ -943,6 +955,8 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   }
   std::vector<float2> lj((size_t)T * T);
   for (int t = 0; t < T * T; ++t) lj[t] = make_float2((float)(6.0 * sys->c6[t]), (float)(12.0 * sys->c12[t]));
+  std::vector<double2> lj64((size_t)T * T);     // (c6, c12) in fp64 for the LJ energy
+  for (int t = 0; t < T * T; ++t) lj64[t] = make_double2(sys->c6[t], sys->c12[t]);
   std::vector<float> bsp;
   for (int dd = 0; dd < 3; ++dd) bsp_moduli(kp.K[dd], bsp);
   std::vector<double> lam0((size_t)R * C, 0.0);
@@ -972,6 +986,7 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
       UP(d.excl_ptr, c.h_excl_ptr.data(), N + 1);
       if (!c.h_excl_idx.empty()) UP(d.excl_idx, c.h_excl_idx.data(), c.h_excl_idx.size());
       UP(d.ljtab, lj.data(), lj.size());
+      UP(d.ljtab64, lj64.data(), lj64.size());
       UP(d.bsp, bsp.data(), bsp.size());
       if (G) {
         UP(d.g_kind, c.h_group_kind.data(), G); UP(d.g_ptr, c.h_group_ptr.data(), G + 1);
@@ -1857,7 +1872,9 @@ static cph_status set_states(Ctx &c, int r0, int nr, const void *buf, int64_t nb
   if (st) return st;
   CK(cudaStreamSynchronize(c.stream));
   if ((st = set_states_rejected(c)) || (st = set_states_apply(c, r0, nr, step))) return st;
-  return check_flags(c);
+  // the re-evaluation is enqueued, not awaited: a device-side failure in it (list overflow,
+  // divergence) is latched and reported by the next call, as for cph_step
+  return CPH_OK;
 }
 
 static cph_status sub_get_state(SubCtx *ctx, int32_t r, void *buf, int64_t cap, int64_t *n) {
@@ -2464,8 +2481,7 @@ cph_status cph_set_state_all(cph_ctx *ctx, const void *buf, int64_t nbytes) {
     Ctx &c = ctx->sub[s]->c;
     if ((st = fwd(ctx, (int)s, set_states_apply(c, 0, c.kp.R, steps[s])))) return st;
   }
-  for (size_t s = 0; s < S; ++s)
-    if ((st = fwd(ctx, (int)s, check_flags(ctx->sub[s]->c)))) return st;
+  // re-evaluations enqueued on every sub-batch; their device-side flags are checked by the next call
   return join_out(ctx);
 }
 
