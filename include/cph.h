@@ -96,7 +96,7 @@ typedef struct {
   const double *c12;            /* [T*T] kJ mol^-1 nm^12, symmetric */
   int32_t n_excl;               /* number of excluded pairs */
   const int32_t *excl;          /* [2*n_excl] unordered atom pairs, i != j */
-  double box[3];                /* rectangular box edges, nm */
+  double box[3];                /* rectangular box edges, nm; the device simulates fl32(box) (R34) */
   int32_t n_groups;             /* G >= 0 lambda-groups */
   const int32_t *group_kind;    /* [G] 2 (one coordinate) or 3 (two coordinates) */
   const int32_t *group_ptr;     /* [G+1] CSR offsets into group_atoms */

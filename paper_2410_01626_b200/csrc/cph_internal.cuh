@@ -108,7 +108,6 @@ struct DevBufs {
   int *nnb = nullptr;                               // [R*Nst]
   int *excl_ptr = nullptr, *excl_idx = nullptr;     // CSR by original atom
   float2 *ljtab = nullptr;                          // [T*T] (6 c6, 12 c12) fp32
-  double2 *ljtab64 = nullptr;                       // [T*T] (c6, c12) fp64: LJ energy on energy steps
   double *phi64_nb = nullptr;                       // [R*nlam]
   float *grid = nullptr;                            // [R*K3]
   float2 *cgrid = nullptr;                          // [R*Kc]

@@ -867,7 +867,6 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   d.excl_ptr = dalloc<int>(c, N + 1);
   d.excl_idx = dalloc<int>(c, c.h_excl_idx.size());
   d.ljtab = dalloc<float2>(c, (size_t)T * T);
-  d.ljtab64 = dalloc<double2>(c, (size_t)T * T);
   d.phi64_nb = dalloc<double>(c, (size_t)R * nlam);
   d.phi_lam = dalloc<double>(c, (size_t)R * nlam);
   d.grid = dalloc<float>(c, (size_t)R * kp.K3);
@@ -955,8 +954,6 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   }
   std::vector<float2> lj((size_t)T * T);
   for (int t = 0; t < T * T; ++t) lj[t] = make_float2((float)(6.0 * sys->c6[t]), (float)(12.0 * sys->c12[t]));
-  std::vector<double2> lj64((size_t)T * T);     // (c6, c12) in fp64 for the LJ energy
-  for (int t = 0; t < T * T; ++t) lj64[t] = make_double2(sys->c6[t], sys->c12[t]);
   std::vector<float> bsp;
   for (int dd = 0; dd < 3; ++dd) bsp_moduli(kp.K[dd], bsp);
   std::vector<double> lam0((size_t)R * C, 0.0);
@@ -986,7 +983,6 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
       UP(d.excl_ptr, c.h_excl_ptr.data(), N + 1);
       if (!c.h_excl_idx.empty()) UP(d.excl_idx, c.h_excl_idx.data(), c.h_excl_idx.size());
       UP(d.ljtab, lj.data(), lj.size());
-      UP(d.ljtab64, lj64.data(), lj64.size());
       UP(d.bsp, bsp.data(), bsp.size());
       if (G) {
         UP(d.g_kind, c.h_group_kind.data(), G); UP(d.g_ptr, c.h_group_ptr.data(), G + 1);
@@ -1908,9 +1904,9 @@ static cph_status sub_get_state_all(SubCtx *ctx, void *buf, int64_t cap, int64_t
   if (!buf) return CPH_OK;
   if (cap < *n) { c.err = "state buffer too small"; return CPH_E_INVALID; }
   cudaSetDevice(c.device);
-  cph_status st = sub_sync(ctx);
+  cph_status st = get_states_enqueue(c, 0, c.kp.R, buf);   // behind the queued work; flags checked after
   if (st) return st;
-  return get_states(c, 0, c.kp.R, buf);
+  return sub_sync(ctx);
 }
 
 static cph_status sub_set_state_all(SubCtx *ctx, const void *buf, int64_t nbytes) {
@@ -2418,19 +2414,15 @@ cph_status cph_get_state_all(cph_ctx *ctx, void *buf, int64_t cap, int64_t *n) {
   if (!buf) return CPH_OK;
   if (cap < *n) { ctx->err = "state buffer too small"; return CPH_E_INVALID; }
   cudaSetDevice(ctx->device);
-  // latched errors first; then every sub-batch packs and copies out side by side
-  for (size_t s = 0; s < ctx->sub.size(); ++s)
-    if (cph_status st = fwd(ctx, (int)s, sub_sync(ctx->sub[s]))) return st;
+  // every sub-batch packs and copies out behind its queued work, side by side (a batch's copy
+  // overlaps the others' compute); latched device failures are checked once all have landed
   for (size_t s = 0; s < ctx->sub.size(); ++s) {
     Ctx &c = ctx->sub[s]->c;
     if (cph_status st = fwd(ctx, (int)s, get_states_enqueue(c, 0, c.kp.R, (char *)buf + one * ctx->first[s])))
       return st;
   }
   for (size_t s = 0; s < ctx->sub.size(); ++s)
-    if (cudaStreamSynchronize(ctx->sub[s]->c.stream) != cudaSuccess) {
-      ctx->err = "cudaStreamSynchronize failed";
-      return CPH_E_CUDA;
-    }
+    if (cph_status st = fwd(ctx, (int)s, sub_sync(ctx->sub[s]))) return st;
   return CPH_OK;
 }
 

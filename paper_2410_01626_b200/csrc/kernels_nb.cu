@@ -28,12 +28,6 @@ constexpr bool kNbPacked = CPH_NB_PACKED;
 #define CPH_NB_MINB 7   // CTAs per SM the register budget is sized for (A/B: 6 and 8 slower)
 #endif
 
-// c12 / r^12 - c6 / r^6 in fp64 from the fp32 r^2 and the fp64 (c6, c12)
-__device__ __forceinline__ double lj_energy64(float r2, double2 c) {
-  const double ir2 = 1.0 / (double)r2, ir6 = ir2 * ir2 * ir2;
-  return ir6 * (c.y * ir6 - c.x);
-}
-
 template <bool ENERGY, bool PHI64>
 __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, const float4 *__restrict__ xq,
                                         const float2 *__restrict__ ljf, const float2 *__restrict__ lje,
@@ -48,6 +42,7 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
   const uint4 *L = reinterpret_cast<const uint4 *>(d.nbl + (size_t)r * kp.cap * kp.Nst) + 2 * (size_t)i;
   const size_t tstride = 2 * (size_t)kp.Nst;
   const float2 *ljrow = ljf + ti * kp.T;
+  const float2 *ljerow = lje + ti * kp.T;
   const float rc2 = kp.rc2, beta = kp.beta, c2b = kp.two_beta_sqrtpi;
   const float kexp = -kp.beta * kp.beta * 1.4426950408889634f;   // exp(-b^2 r^2) = 2^(kexp r^2)
   const float pbeta = kErfcP * kp.beta;
@@ -89,11 +84,8 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
       fz = fmaf(fs, dz, fz);
       if (PHI64 || ENERGY) phid += (double)qe;
       if (ENERGY) {
-        // energy steps only: the LJ energy in fp64 from the fp32 r^2 and fp64 parameters (the
-        // fp32 table's rounding is one-signed per type pair, and the cancelling repulsive and
-        // dispersive sums amplify it to ~3e-6 of E_LJ against the 1e-6 E_total bar)
-        const double2 ce = d.ljtab64[ti * kp.T + (int)((e[u] >> kEntryTypeShift) & kEntryTypeMask)];
-        elj += in ? lj_energy64(r2, ce) : 0.0;
+        const float2 ce = ljerow[(e[u] >> kEntryTypeShift) & kEntryTypeMask];   // (c6, c12)
+        elj += in ? (double)(r6 * fmaf(ce.y, r6, -ce.x)) : 0.0;
       }
     }
   };
@@ -538,9 +530,9 @@ __device__ __forceinline__ void nb_cluster_warp(const KParams &kp, const DevBufs
       gy = __ffma2_rn(fs, dy, gy);
       gz = __ffma2_rn(fs, dz, gz);
       if (ENERGY) {
-        const double2 ca = d.ljtab64[trow[2 * P] + tj], cb = d.ljtab64[trow[2 * P + 1] + tj];   // (c6, c12)
-        elj += ina ? lj_energy64(r2.x, ca) : 0.0;
-        elj += inb ? lj_energy64(r2.y, cb) : 0.0;
+        const float2 ca = s_lje[trow[2 * P] + tj], cb = s_lje[trow[2 * P + 1] + tj];   // (c6, c12)
+        elj += ina ? (double)(r6.x * fmaf(ca.y, r6.x, -ca.x)) : 0.0;
+        elj += inb ? (double)(r6.y * fmaf(cb.y, r6.y, -cb.x)) : 0.0;
         ere += (double)qif[P].x * (double)(qj * er.x) + (double)qif[P].y * (double)(qj * er.y);
       }
     }

@@ -198,7 +198,9 @@ def make_system(cfg: int, seed: int | None = None, n_target: int | None = None) 
     """Build configuration `cfg` (1..5) deterministically from `seed` (default 1000*cfg)."""
     spec = CONFIGS[cfg]
     rng = np.random.default_rng(1000 * cfg if seed is None else seed)
-    L = float(spec["L"])
+    # the box edge is an fp32 value: the device stores and wraps coordinates in fp32 with
+    # fl32(L), so the oracle (fp64) and the device then simulate the same box (DESIGN.md R34)
+    L = float(np.float32(spec["L"]))
     n_target = spec["n"] if n_target is None else n_target
     box = np.array([L, L, L], dtype=np.float64)
 

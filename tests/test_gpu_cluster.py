@@ -89,3 +89,20 @@ def test_deterministic_rejects_cluster(cph):
     s = small_system()
     with pytest.raises(cph.CphError):
         cph.cph_create(s, [4.0], [1], pair_list=2, deterministic=1)
+
+
+def test_cluster_pairlist_rows_c4(cph):
+    """C4 (40k atoms, the bench config): sampled full rows of the cluster list (2000 atoms incl.
+    every lambda atom and solute exclusions) against the oracle's canonical rows, at create and
+    after a rebuild."""
+    s = make_system(4)
+    ctx = cph.cph_create(s, [5.0], [11], vel_replicas=make_velocities(s, 3)[None], pair_list=2)
+    rng = np.random.default_rng(4)
+    idx = np.unique(np.concatenate([s.group_atoms, s.excl[:200, 0], rng.choice(s.n_atoms, 1800, replace=False)]))
+    for stage in range(2):
+        x = s.pos if stage == 0 else ctx.cph_get_positions(0)[0]
+        got = ctx.cph_get_pairlist_rows(0, idx)
+        ref = OPL.canonical_partners(x, s.box, s.params["rlist"], s.excl, idx)
+        bad = [int(i) for i, a, b in zip(idx, got, ref) if not np.array_equal(a, b)]
+        assert not bad, bad[:10]
+        ctx.cph_step(s.params["nstlist"])
