@@ -54,6 +54,7 @@ struct KParams {
   int ns[3], so[3];            // stencil sizes and first offsets per dimension
   int nb_packed;               // pair kernel: FFMA2 path for non-lambda warps (A/B: CPH_NB_PACKED=0)
   int det;                     // deterministic (fixed-point) PME spread
+  int fft64;                   // small grids (K^3 <= 32768): PME grid, FFTs and solve in fp64
   // list
   int cap;                     // neighbour capacity per atom (per-atom list; lambda-atom lists)
   int pair_mode;               // 0 per-atom full list, 1 cluster-pair list (cph_params.pair_list)
@@ -113,6 +114,9 @@ struct DevBufs {
   float2 *cgrid = nullptr;                          // [R*Kc]
   float *bsp = nullptr;                             // [Kx + Ky + Kz] |b|^2 moduli
   float *ginf = nullptr;                            // [Kc] influence function G(m) (replica independent)
+  double *grid64 = nullptr;                         // [R*K3] fp64 grid (fft64 mode)
+  double2 *cgrid64 = nullptr;                       // [R*Kc] fp64 half spectrum (fft64 mode)
+  double *ginf64 = nullptr;                         // [Kc] fp64 G(m) (fft64 mode)
   unsigned long long *grid_fx = nullptr;            // [R*K3] fixed-point spread accumulator (deterministic mode)
   int *g_kind = nullptr, *g_ptr = nullptr, *g_atoms = nullptr, *g_cptr = nullptr;
   double *g_q = nullptr;                            // [nlam*4]
@@ -228,6 +232,7 @@ int launch_spread(Ctx &c, cudaStream_t s);
 int launch_solve(Ctx &c, cudaStream_t s, int step_offset);
 int launch_influence(Ctx &c, cudaStream_t s);                      // G(m) table, once at create
 int launch_gather(Ctx &c, cudaStream_t s);
+int launch_grid_to32(Ctx &c, cudaStream_t s);                      // fft64 mode: grid64 -> grid after the back transform
 int launch_lambda_reduce(Ctx &c, cudaStream_t s, int mode);       // 0 init eval, 1 step
 int launch_lambda_open(Ctx &c, cudaStream_t s);
 int launch_set_charges(Ctx &c, cudaStream_t s);

@@ -253,6 +253,16 @@ static void tl_print(Ctx &c) {
   }
 }
 
+// the PME transforms (fp32, or fp64 on small grids: kp.fft64), on the plans' current stream
+static cufftResult fft_forward(Ctx &c) {
+  if (c.kp.fft64) return cufftExecD2Z(c.plan_r2c, c.d.grid64, (cufftDoubleComplex *)c.d.cgrid64);
+  return cufftExecR2C(c.plan_r2c, c.d.grid, (cufftComplex *)c.d.cgrid);
+}
+static cufftResult fft_backward(Ctx &c) {
+  if (c.kp.fft64) return cufftExecZ2D(c.plan_c2r, (cufftDoubleComplex *)c.d.cgrid64, c.d.grid64);
+  return cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid);
+}
+
 // one full step (n -> n+1) on the context streams; returns kernels launched
 int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
   CPH_NVTX(rebuild ? "cph step (rebuild)" : "cph step");
@@ -277,11 +287,12 @@ int enqueue_step(Ctx &c, bool rebuild, bool two_streams) {
   cufftSetStream(c.plan_c2r, sp);
   k += launch_spread(c, sp);
   tl_mark(c, sp, 4);
-  cufftExecR2C(c.plan_r2c, c.d.grid, (cufftComplex *)c.d.cgrid);
+  fft_forward(c);
   tl_mark(c, sp, 5);
   k += launch_solve(c, sp, 1);
   tl_mark(c, sp, 6);
-  cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid);
+  fft_backward(c);
+  k += launch_grid_to32(c, sp);
   tl_mark(c, sp, 7);
   k += launch_hi_recip(c, sp);
   // the lambda kernel reads phi_rec of its atoms straight from the grid: it waits for the
@@ -361,9 +372,10 @@ cph_status evaluate_here(Ctx &c, bool rebuild) {
   cufftSetStream(c.plan_r2c, sp);
   cufftSetStream(c.plan_c2r, sp);
   k += launch_spread(c, sp);
-  CKF(cufftExecR2C(c.plan_r2c, c.d.grid, (cufftComplex *)c.d.cgrid));
+  CKF(fft_forward(c));
   k += launch_solve(c, sp, 0);
-  CKF(cufftExecC2R(c.plan_c2r, (cufftComplex *)c.d.cgrid, c.d.grid));
+  CKF(fft_backward(c));
+  k += launch_grid_to32(c, sp);
   k += launch_gather(c, sp);
   k += launch_hi_recip(c, sp);
   if (!one) CK(cudaEventRecord(c.ev_join, sp));
@@ -729,6 +741,8 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   }
   for (int d = 0; d < 3; ++d) kp.K[d] = prm->pme_grid[d];
   kp.K3 = kp.K[0] * kp.K[1] * kp.K[2];
+  kp.fft64 = kp.K3 <= 32768;   // small grids: fp64 PME grid / transforms (kernels_pme.cu k_spread64)
+  if (getenv("CPH_FFT64")) kp.fft64 = atoi(getenv("CPH_FFT64"));
   kp.Kzc = kp.K[2] / 2 + 1;
   kp.Kc = kp.K[0] * kp.K[1] * kp.Kzc;
   kp.dtd = prm->dt;
@@ -873,6 +887,12 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   d.cgrid = dalloc<float2>(c, (size_t)R * kp.Kc);
   d.bsp = dalloc<float>(c, kp.K[0] + kp.K[1] + kp.K[2]);
   d.ginf = dalloc<float>(c, kp.Kc);
+  if (kp.fft64) {
+    d.grid64 = dalloc<double>(c, (size_t)R * kp.K3);
+    d.cgrid64 = dalloc<double2>(c, (size_t)R * kp.Kc);
+    d.ginf64 = dalloc<double>(c, kp.Kc);
+    if (!d.grid64 || !d.cgrid64 || !d.ginf64) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
+  }
   if (kp.det) {
     d.grid_fx = dalloc<unsigned long long>(c, (size_t)R * kp.K3);
     if (!d.grid_fx) { c.err = "device allocation failed"; return fail_create(ctx, CPH_E_OOM); }
@@ -1030,8 +1050,10 @@ static cph_status sub_create(const cph_system *sys, const cph_params *prm, SubCt
   // cuFFT plans (batched over replicas)
   {
     int n3[3] = {kp.K[0], kp.K[1], kp.K[2]};
-    if (cufftPlanMany(&c.plan_r2c, 3, n3, nullptr, 1, kp.K3, nullptr, 1, kp.Kc, CUFFT_R2C, R) != CUFFT_SUCCESS ||
-        cufftPlanMany(&c.plan_c2r, 3, n3, nullptr, 1, kp.Kc, nullptr, 1, kp.K3, CUFFT_C2R, R) != CUFFT_SUCCESS) {
+    if (cufftPlanMany(&c.plan_r2c, 3, n3, nullptr, 1, kp.K3, nullptr, 1, kp.Kc, kp.fft64 ? CUFFT_D2Z : CUFFT_R2C, R) !=
+            CUFFT_SUCCESS ||
+        cufftPlanMany(&c.plan_c2r, 3, n3, nullptr, 1, kp.Kc, nullptr, 1, kp.K3, kp.fft64 ? CUFFT_Z2D : CUFFT_C2R, R) !=
+            CUFFT_SUCCESS) {
       c.err = "cufftPlanMany failed";
       return fail_create(ctx, CPH_E_CUDA);
     }
@@ -1977,13 +1999,13 @@ static cph_status profile_batches(const std::vector<Ctx *> &cs, const std::vecto
     phase(CPH_K_NONBONDED, [&](Ctx &x, cudaStream_t s) { return launch_nonbonded(x, s, 1); });
     phase(CPH_K_SPREAD, [&](Ctx &x, cudaStream_t s) { return launch_spread(x, s); });
     phase(CPH_K_FFT_R2C, [&](Ctx &x, cudaStream_t) {
-      cufftExecR2C(x.plan_r2c, x.d.grid, (cufftComplex *)x.d.cgrid);
+      fft_forward(x);
       return 0;
     });
     phase(CPH_K_SOLVE, [&](Ctx &x, cudaStream_t s) { return launch_solve(x, s, 1); });
-    phase(CPH_K_FFT_C2R, [&](Ctx &x, cudaStream_t) {
-      cufftExecC2R(x.plan_c2r, (cufftComplex *)x.d.cgrid, x.d.grid);
-      return 0;
+    phase(CPH_K_FFT_C2R, [&](Ctx &x, cudaStream_t s) {
+      fft_backward(x);
+      return launch_grid_to32(x, s);
     });
     phase(CPH_K_GATHER, [&](Ctx &x, cudaStream_t s) { return launch_gather(x, s); });
     if (c.kp.hi)

@@ -114,9 +114,97 @@ __global__ void __launch_bounds__(128) k_spread_fx(KParams kp, DevBufs d) {
 __global__ void __launch_bounds__(256) k_fx_to_float(KParams kp, DevBufs d) {
   const size_t n = (size_t)kp.R * kp.K3;
   for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
-    d.grid[t] = (float)((double)(long long)d.grid_fx[t] * kFxInv);
+    const double v = (double)(long long)d.grid_fx[t] * kFxInv;
+    if (kp.fft64) d.grid64[t] = v;
+    else d.grid[t] = (float)v;
     d.grid_fx[t] = 0ull;
   }
+}
+
+// Small grids (kp.fft64, K^3 <= 32768: tiny test systems and C1, where the transforms cost
+// microseconds): the same B-spline contributions added in fp64 (native fp64 atomics), fp64
+// transforms and solve, and the back-transformed grid rounded once to fp32 for the gather and
+// the lambda kernel.  The fp32 transforms' ~3e-7 relative error of E_rec otherwise dominates the
+// 1e-6 E_total bar when the total is a small difference of the self, reciprocal and real terms.
+__global__ void __launch_bounds__(128) k_spread64(KParams kp, DevBufs d) {
+  const int r = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= kp.N) return;
+  const float4 p = d.xyzq[(size_t)r * kp.Nst + i];
+  if (p.w == 0.0f) return;
+  int kx, ky, kz;
+  float tx[4], ty[4], tz[4], dd[4];
+  bspline4(p.x, kp.invL[0], kp.K[0], kx, tx, dd);
+  bspline4(p.y, kp.invL[1], kp.K[1], ky, ty, dd);
+  bspline4(p.z, kp.invL[2], kp.K[2], kz, tz, dd);
+  double *g = d.grid64 + (size_t)r * kp.K3;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int ix = (kx - a + kp.K[0]) % kp.K[0];
+    const float qa = p.w * tx[a];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int iy = (ky - b + kp.K[1]) % kp.K[1];
+      const float qab = qa * ty[b];
+      double *row = g + ((size_t)ix * kp.K[1] + iy) * kp.K[2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) atomicAdd(row + (kz - c + kp.K[2]) % kp.K[2], (double)(qab * tz[c]));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_influence64(KParams kp, DevBufs d) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= kp.Kc) return;
+  const int mz = idx % kp.Kzc;
+  const int t = idx / kp.Kzc;
+  const int my = t % kp.K[1];
+  const int mx = t / kp.K[1];
+  const double fx = (double)(mx <= kp.K[0] / 2 ? mx : mx - kp.K[0]) / kp.Ld[0];
+  const double fy = (double)(my <= kp.K[1] / 2 ? my : my - kp.K[1]) / kp.Ld[1];
+  const double fz = (double)mz / kp.Ld[2];
+  const double m2 = fx * fx + fy * fy + fz * fz;
+  double G = 0.0;
+  if (idx != 0) {
+    const double V = kp.Ld[0] * kp.Ld[1] * kp.Ld[2];
+    G = exp(-kPi * kPi * m2 / (kp.beta_d * kp.beta_d)) / (kPi * V * m2) * (double)d.bsp[mx] *
+        (double)d.bsp[kp.K[0] + my] * (double)d.bsp[kp.K[0] + kp.K[1] + mz];
+  }
+  d.ginf64[idx] = G;
+}
+
+__global__ void __launch_bounds__(256) k_solve64(KParams kp, DevBufs d, int step_offset) {
+  const int r = blockIdx.y;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long m = *d.step + step_offset;
+  const bool energy = is_energy_step(m, *d.end_step, kp.nstenergy);
+  double e = 0.0;
+  if (idx < kp.Kc) {
+    const double G = d.ginf64[idx];
+    double2 *cg = d.cgrid64 + (size_t)r * kp.Kc + idx;
+    double2 c = *cg;
+    if (energy) {
+      const int mz = idx % kp.Kzc;
+      const double w = (mz == 0 || (2 * mz == kp.K[2])) ? 1.0 : 2.0;
+      e = w * G * (c.x * c.x + c.y * c.y);
+    }
+    c.x *= G;
+    c.y *= G;
+    *cg = c;
+  }
+  if (energy) block_atomic_add_d(0.5 * kFCoul * e, d.erec + ((size_t)(m & 1) * kp.R + r) * kNE + CPH_E_RECIP);
+}
+
+__global__ void __launch_bounds__(256) k_grid_to32(KParams kp, DevBufs d) {
+  const size_t n = (size_t)kp.R * kp.K3;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x)
+    d.grid[t] = (float)d.grid64[t];
+}
+
+int launch_grid_to32(Ctx &c, cudaStream_t s) {
+  if (!c.kp.fft64) return 0;
+  const size_t n = (size_t)c.kp.R * c.kp.K3;
+  k_grid_to32<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(c.kp, c.d);
+  return 1;
 }
 
 // Influence function G(m) = exp(-pi^2 m^2/beta^2)/(pi V m^2) |b_x|^2 |b_y|^2 |b_z|^2 on the
@@ -168,7 +256,8 @@ __global__ void __launch_bounds__(256) k_solve(KParams kp, DevBufs d, int step_o
 
 int launch_influence(Ctx &c, cudaStream_t s) {
   k_influence<<<(c.kp.Kc + 255) / 256, 256, 0, s>>>(c.kp, c.d);
-  return 1;
+  if (c.kp.fft64) k_influence64<<<(c.kp.Kc + 255) / 256, 256, 0, s>>>(c.kp, c.d);
+  return c.kp.fft64 ? 2 : 1;
 }
 
 // forces on every atom (and the fp32 phi_rec reported by cph_get_forces); the fp64 phi_rec of
@@ -369,6 +458,11 @@ int launch_spread(Ctx &c, cudaStream_t s) {
     k_fx_to_float<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(c.kp, c.d);
     return 2;
   }
+  if (c.kp.fft64) {
+    cudaMemsetAsync(c.d.grid64, 0, sizeof(double) * (size_t)c.kp.R * c.kp.K3, s);
+    k_spread64<<<dim3((c.kp.N + 127) / 128, c.kp.R), 128, 0, s>>>(c.kp, c.d);
+    return 1;
+  }
   cudaMemsetAsync(c.d.grid, 0, sizeof(float) * (size_t)c.kp.R * c.kp.K3, s);
   dim3 grid((c.kp.N + CPH_SPREAD_TPB - 1) / CPH_SPREAD_TPB, c.kp.R);
   k_spread<<<grid, CPH_SPREAD_TPB, 0, s>>>(c.kp, c.d);
@@ -376,7 +470,8 @@ int launch_spread(Ctx &c, cudaStream_t s) {
 }
 int launch_solve(Ctx &c, cudaStream_t s, int step_offset) {
   dim3 grid((c.kp.Kc + 255) / 256, c.kp.R);
-  k_solve<<<grid, 256, 0, s>>>(c.kp, c.d, step_offset);
+  if (c.kp.fft64) k_solve64<<<grid, 256, 0, s>>>(c.kp, c.d, step_offset);
+  else k_solve<<<grid, 256, 0, s>>>(c.kp, c.d, step_offset);
   return 1;
 }
 int launch_gather(Ctx &c, cudaStream_t s) {
