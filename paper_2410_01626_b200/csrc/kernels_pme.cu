@@ -121,37 +121,11 @@ __global__ void __launch_bounds__(256) k_fx_to_float(KParams kp, DevBufs d) {
   }
 }
 
-// Small grids (kp.fft64, K^3 <= 32768: tiny test systems and C1, where the transforms cost
-// microseconds): the same B-spline contributions added in fp64 (native fp64 atomics), fp64
-// transforms and solve, and the back-transformed grid rounded once to fp32 for the gather and
-// the lambda kernel.  The fp32 transforms' ~3e-7 relative error of E_rec otherwise dominates the
-// 1e-6 E_total bar when the total is a small difference of the self, reciprocal and real terms.
-__global__ void __launch_bounds__(128) k_spread64(KParams kp, DevBufs d) {
-  const int r = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= kp.N) return;
-  const float4 p = d.xyzq[(size_t)r * kp.Nst + i];
-  if (p.w == 0.0f) return;
-  int kx, ky, kz;
-  float tx[4], ty[4], tz[4], dd[4];
-  bspline4(p.x, kp.invL[0], kp.K[0], kx, tx, dd);
-  bspline4(p.y, kp.invL[1], kp.K[1], ky, ty, dd);
-  bspline4(p.z, kp.invL[2], kp.K[2], kz, tz, dd);
-  double *g = d.grid64 + (size_t)r * kp.K3;
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int ix = (kx - a + kp.K[0]) % kp.K[0];
-    const float qa = p.w * tx[a];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int iy = (ky - b + kp.K[1]) % kp.K[1];
-      const float qab = qa * ty[b];
-      double *row = g + ((size_t)ix * kp.K[1] + iy) * kp.K[2];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) atomicAdd(row + (kz - c + kp.K[2]) % kp.K[2], (double)(qab * tz[c]));
-    }
-  }
-}
-
+// Small grids (kp.fft64, K^3 <= 32768: tiny test systems and C1): the fp32 spread grid widened
+// to fp64 (k_grid_to64), fp64 transforms and solve, and the back-transformed grid rounded once to
+// fp32 for the gather and the lambda kernel.  The fp32 transforms' ~3e-7 relative error of E_rec
+// otherwise dominates the 1e-6 E_total bar when the total is a small difference of the self,
+// reciprocal and real-space terms.
 __global__ void __launch_bounds__(256) k_influence64(KParams kp, DevBufs d) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= kp.Kc) return;
@@ -198,6 +172,12 @@ __global__ void __launch_bounds__(256) k_grid_to32(KParams kp, DevBufs d) {
   const size_t n = (size_t)kp.R * kp.K3;
   for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x)
     d.grid[t] = (float)d.grid64[t];
+}
+
+__global__ void __launch_bounds__(256) k_grid_to64(KParams kp, DevBufs d) {
+  const size_t n = (size_t)kp.R * kp.K3;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x)
+    d.grid64[t] = (double)d.grid[t];
 }
 
 int launch_grid_to32(Ctx &c, cudaStream_t s) {
@@ -459,9 +439,11 @@ int launch_spread(Ctx &c, cudaStream_t s) {
     return 2;
   }
   if (c.kp.fft64) {
-    cudaMemsetAsync(c.d.grid64, 0, sizeof(double) * (size_t)c.kp.R * c.kp.K3, s);
-    k_spread64<<<dim3((c.kp.N + 127) / 128, c.kp.R), 128, 0, s>>>(c.kp, c.d);
-    return 1;
+    cudaMemsetAsync(c.d.grid, 0, sizeof(float) * (size_t)c.kp.R * c.kp.K3, s);
+    k_spread<<<dim3((c.kp.N + CPH_SPREAD_TPB - 1) / CPH_SPREAD_TPB, c.kp.R), CPH_SPREAD_TPB, 0, s>>>(c.kp, c.d);
+    const size_t n = (size_t)c.kp.R * c.kp.K3;
+    k_grid_to64<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(c.kp, c.d);
+    return 2;
   }
   cudaMemsetAsync(c.d.grid, 0, sizeof(float) * (size_t)c.kp.R * c.kp.K3, s);
   dim3 grid((c.kp.N + CPH_SPREAD_TPB - 1) / CPH_SPREAD_TPB, c.kp.R);
