@@ -24,6 +24,10 @@ namespace cph {
 #endif
 constexpr bool kNbPacked = CPH_NB_PACKED;
 
+#ifndef CPH_NB_R2CLAMP
+#define CPH_NB_R2CLAMP 1   // packed path: out-of-range entries via r^2 = 1e30 instead of two selects (A/B switch)
+#endif
+
 #ifndef CPH_NB_MINB
 #define CPH_NB_MINB 7   // CTAs per SM the register budget is sized for (A/B: 6 and 8 slower)
 #endif
@@ -227,13 +231,21 @@ __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, 
     const float2 qa = __fmul2_rn(da, da), qb = __fmul2_rn(db, db);
     const float2 r2 = f2(fmaf(dza, dza, qa.x + qa.y), fmaf(dzb, dzb, qb.x + qb.y));
     const bool ina = (r2.x < rc2) && (r2.x > 0.0f), inb = (r2.y < rc2) && (r2.y > 0.0f);
-    const float2 rinv = f2(rsqrtf(r2.x), rsqrtf(r2.y));
+#if CPH_NB_R2CLAMP
+    // an entry outside (0, r_c) gets r^2 = 1e30: e^{-b^2 r^2}, r^-6 (flushed) and hence its
+    // potential and force come out exactly zero, so the two selects per entry after the
+    // arithmetic are not needed (ALU pipe; same sums as masking)
+    const float2 r2m = f2(ina ? r2.x : 1e30f, inb ? r2.y : 1e30f);
+#else
+    const float2 r2m = r2;
+#endif
+    const float2 rinv = f2(rsqrtf(r2m.x), rsqrtf(r2m.y));
     const float2 r2inv = __fmul2_rn(rinv, rinv);
     const float2 r6 = __fmul2_rn(__fmul2_rn(r2inv, r2inv), r2inv);
     const float2 flj = __fmul2_rn(r6, __ffma2_rn(c12, r6, c6));
-    const float2 den = __ffma2_rn(pbeta2, __fmul2_rn(r2, rinv), one2);
+    const float2 den = __ffma2_rn(pbeta2, __fmul2_rn(r2m, rinv), one2);
     const float2 t = f2(__fdividef(1.0f, den.x), __fdividef(1.0f, den.y));
-    const float2 zz = __fmul2_rn(r2, kexp2);
+    const float2 zz = __fmul2_rn(r2m, kexp2);
     const float2 ez = f2(exp2f(zz.x), exp2f(zz.y));
     const float2 bq = __fmul2_rn(f2(xa.w, xb.w), ez);
     float2 pa = f2(-1.348251700e-01f, -1.348251700e-01f);
@@ -247,8 +259,10 @@ __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, 
     pa = __fmul2_rn(pa, t);                                       // erfc(beta r) exp(beta^2 r^2)
     float2 qe = __fmul2_rn(__fmul2_rn(pa, bq), rinv);             // q_j erfc(beta r) / r
     float2 fs = __fmul2_rn(__ffma2_rn(qif, __ffma2_rn(c2b2, bq, qe), flj), r2inv);
+#if !CPH_NB_R2CLAMP
     qe = f2(ina ? qe.x : 0.f, inb ? qe.y : 0.f);
     fs = f2(ina ? fs.x : 0.f, inb ? fs.y : 0.f);
+#endif
     phi = __fadd2_rn(phi, qe);
     if (PHI64) phid += (double)qe.x + (double)qe.y;
     fxy = __ffma2_rn(f2(fs.x, fs.x), da, fxy);
