@@ -24,6 +24,10 @@ namespace cph {
 #endif
 constexpr bool kNbPacked = CPH_NB_PACKED;
 
+#ifndef CPH_NB_SMALLT
+#define CPH_NB_SMALLT 1   // T <= 4: the lane's LJ row in registers, FSEL-selected (A/B: 0 = shared-memory table)
+#endif
+
 #ifndef CPH_NB_R2CLAMP
 #define CPH_NB_R2CLAMP 1   // packed path: out-of-range entries via r^2 = 1e30 instead of two selects (A/B switch)
 #endif
@@ -364,14 +368,14 @@ __global__ void __launch_bounds__(128, CPH_NB_MINB) k_nonbonded(KParams kp, DevB
   if (warp_lam) {
     if (energy) nb_atom<true, true>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
     else if (kNbPacked && kp.nb_packed) {
-      if (kp.T <= 4) nb_atom_x2<true, true>(kp, d, xq, s_c6n, s_c12, shn, r, i, valid, xi, ti, lslot, n, nmax);
+      if (CPH_NB_SMALLT && kp.T <= 4) nb_atom_x2<true, true>(kp, d, xq, s_c6n, s_c12, shn, r, i, valid, xi, ti, lslot, n, nmax);
       else nb_atom_x2<true, false>(kp, d, xq, s_c6n, s_c12, shn, r, i, valid, xi, ti, lslot, n, nmax);
     }
     else nb_atom<false, true>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
   } else {
     if (energy) nb_atom<true, false>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
     else if (kNbPacked && kp.nb_packed) {
-      if (kp.T <= 4) nb_atom_x2<false, true>(kp, d, xq, s_c6n, s_c12, shn, r, i, valid, xi, ti, lslot, n, nmax);
+      if (CPH_NB_SMALLT && kp.T <= 4) nb_atom_x2<false, true>(kp, d, xq, s_c6n, s_c12, shn, r, i, valid, xi, ti, lslot, n, nmax);
       else nb_atom_x2<false, false>(kp, d, xq, s_c6n, s_c12, shn, r, i, valid, xi, ti, lslot, n, nmax);
     }
     else nb_atom<false, false>(kp, d, xq, s_ljf, s_lje, s_shift, r, i, valid, xi, ti, lslot, n, nmax, &elj, &ere, &eex);
