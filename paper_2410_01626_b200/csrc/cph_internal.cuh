@@ -26,6 +26,10 @@ constexpr uint32_t kEntryJMask = 0x1FFFFFu;
 constexpr int kEntryTypeShift = 21;
 constexpr uint32_t kEntryTypeMask = 0x1Fu;
 constexpr int kEntryImgShift = 26;
+// padding entries (a lane's last tile, and the tiles past its count) name the atom itself with
+// image code 0, i.e. shifted by a whole box diagonal: r^2 = |L|^2 > r_c^2, so the pair kernel's
+// cutoff test alone discards them
+constexpr uint32_t kPadCode = 0u;
 constexpr int kMaxAtoms = 1 << 21;
 
 // Device-side flags (int array)

@@ -396,9 +396,9 @@ __global__ void __launch_bounds__(32) k_build_list(KParams kp, DevBufs d) {
       tc = tn;
     }
     if (valid && cnt > flushed && flushed < kp.cap) {
-      // pad the last tile with the atom's own slot (zero shift, r = 0: skipped by the pair kernel)
+      // pad the last tile with the atom's own slot at image kPadCode (a box diagonal away: r > r_c, skipped)
       const uint32_t self = (uint32_t)i | ((uint32_t)(meta[i].y & (int)kEntryTypeMask) << kEntryTypeShift) |
-                            (13u << kEntryImgShift);
+                            (kPadCode << kEntryImgShift);
       const int h = flushed & 8;
       for (int k = cnt - flushed; k < 8; ++k) s_buf[h + k][lane] = self;
       out[0] = make_uint4(s_buf[h][lane], s_buf[h + 1][lane], s_buf[h + 2][lane], s_buf[h + 3][lane]);
@@ -633,9 +633,9 @@ __global__ void __launch_bounds__(32 * kColWarps) k_build_list_col(KParams kp, D
       }
     }
     if (valid && cnt > flushed && flushed < kp.cap) {
-      // pad the last tile with the atom's own slot (zero shift, r = 0: skipped by the pair kernel)
+      // pad the last tile with the atom's own slot at image kPadCode (a box diagonal away: r > r_c, skipped)
       const uint32_t self = (uint32_t)i | ((uint32_t)(meta[i].y & (int)kEntryTypeMask) << kEntryTypeShift) |
-                            (13u << kEntryImgShift);
+                            (kPadCode << kEntryImgShift);
       uint32_t *t = ring + (flushed & (kRing - 1)) * 32;
       for (int k = cnt - flushed; k < 8; ++k) t[k * 32] = self;
       out[0] = make_uint4(t[0], t[32], t[64], t[96]);

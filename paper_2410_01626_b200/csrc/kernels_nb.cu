@@ -55,11 +55,11 @@ __device__ __forceinline__ void nb_atom(const KParams &kp, const DevBufs &d, con
   const float kexp = -kp.beta * kp.beta * 1.4426950408889634f;   // exp(-b^2 r^2) = 2^(kexp r^2)
   const float pbeta = kErfcP * kp.beta;
   constexpr int U = 4;                 // neighbours in flight per lane (half a list tile)
-  // Entries past a lane's own (padded) count point at the lane's own atom with zero shift
-  // (r2 = 0, masked), so the loads are unconditional; a whole tile (32 bytes per lane, one
+  // Entries past a lane's own (padded) count point at the lane's own atom a box diagonal away
+  // (kPadCode: r > r_c, masked), so the loads are unconditional; a whole tile (32 bytes per lane, one
   // sector) is fetched at once and the next tile is prefetched while this one computes.
   const uint32_t self = (uint32_t)(valid ? i : 0) | ((uint32_t)ti << kEntryTypeShift) |
-                        (13u << kEntryImgShift);
+                        (kPadCode << kEntryImgShift);
   const uint4 selfv = make_uint4(self, self, self, self);
   uint4 ta = selfv, tb = selfv;
   if (n > 0) { ta = __ldcs(L); tb = __ldcs(L + 1); }
@@ -207,7 +207,7 @@ __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, 
   const float2 pbeta2 = f2(kErfcP * kp.beta, kErfcP * kp.beta);
   const float2 c2b2 = f2(kp.two_beta_sqrtpi, kp.two_beta_sqrtpi);
   const float2 one2 = f2(1.f, 1.f);
-  const uint32_t self = (uint32_t)(valid ? i : 0) | ((uint32_t)ti << kEntryTypeShift) | (13u << kEntryImgShift);
+  const uint32_t self = (uint32_t)(valid ? i : 0) | ((uint32_t)ti << kEntryTypeShift) | (kPadCode << kEntryImgShift);
   const uint4 selfv = make_uint4(self, self, self, self);
   uint4 ta = selfv, tb = selfv;
   if (n > 0) { ta = __ldcs(L); tb = __ldcs(L + 1); }
@@ -234,7 +234,7 @@ __device__ __forceinline__ void nb_atom_x2(const KParams &kp, const DevBufs &d, 
     const float dza = (xa.z + sa.z) + nzi, dzb = (xb.z + sb.z) + nzi;
     const float2 qa = __fmul2_rn(da, da), qb = __fmul2_rn(db, db);
     const float2 r2 = f2(fmaf(dza, dza, qa.x + qa.y), fmaf(dzb, dzb, qb.x + qb.y));
-    const bool ina = (r2.x < rc2) && (r2.x > 0.0f), inb = (r2.y < rc2) && (r2.y > 0.0f);
+    const bool ina = r2.x < rc2, inb = r2.y < rc2;        // padding entries: r^2 = |L|^2 (kPadCode)
 #if CPH_NB_R2CLAMP
     // an entry outside (0, r_c) gets r^2 = 1e30: e^{-b^2 r^2}, r^-6 (flushed) and hence its
     // potential and force come out exactly zero, so the two selects per entry after the
