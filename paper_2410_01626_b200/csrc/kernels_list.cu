@@ -442,10 +442,13 @@ __device__ __forceinline__ bool canonical_in_code(float4 xj, float4 xi, float3 L
 // the exclusion test compiled in.  (A 64-entry ring flushed once per staged chunk needed 64 KB
 // of shared memory per CTA, which shrank the L1 of the pair kernels co-running from other
 // replica sub-batches: step +10 %.)
-constexpr int kColWarps = 8;
+// warps per column CTA: 8, or 4 when the mean column holds at most 160 atoms (C1, C2: 94 and 143
+// atoms per column leave half of 8 warps idle; measured C2 x 17 rebuild 0.85 -> 0.71 ms, no change
+// at C4, 16 warps much slower); CPH_COL_WARPS=4|8 forces one
 constexpr int kStage = 36;      // staged candidates per warp: 32 + sentinel padding for aligned groups of 4
 constexpr int kRing = 16;       // per-lane ring: <= 4 accepted per group + 7 pending
 
+template <int kColWarps>
 __global__ void __launch_bounds__(32 * kColWarps) k_build_list_col(KParams kp, DevBufs d) {
   const int r = blockIdx.y, colid = blockIdx.x;
   const int cx = colid / kp.nc[1], cy = colid % kp.nc[1];
@@ -928,7 +931,13 @@ int launch_build_list(Ctx &c, cudaStream_t s) {
   }
   static const bool by_cell = getenv("CPH_BUILD") && getenv("CPH_BUILD")[0] == 'c';   // A/B: one warp per cell
   if (by_cell) k_build_list<<<dim3(c.kp.ncell, c.kp.R), 32, 0, s>>>(c.kp, c.d);
-  else k_build_list_col<<<dim3(c.kp.nc[0] * c.kp.nc[1], c.kp.R), 32 * kColWarps, 0, s>>>(c.kp, c.d);
+  else {
+    const int ncol = c.kp.nc[0] * c.kp.nc[1];
+    static const int force = getenv("CPH_COL_WARPS") ? atoi(getenv("CPH_COL_WARPS")) : 0;
+    const bool small = force ? force == 4 : (double)c.kp.N / ncol <= 160.0;
+    if (small) k_build_list_col<4><<<dim3(ncol, c.kp.R), 32 * 4, 0, s>>>(c.kp, c.d);
+    else k_build_list_col<8><<<dim3(ncol, c.kp.R), 32 * 8, 0, s>>>(c.kp, c.d);
+  }
   return 1;
 }
 

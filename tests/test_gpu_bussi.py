@@ -55,7 +55,7 @@ def test_bussi_temperature_atoms_and_lambda(cph):
     blob = eq.cph_get_state_all()
     ctx = cph.cph_create(s, pH, seeds, vel_replicas=vel, thermostat="bussi", nstenergy=10, barrier=2.0)
     ctx.cph_set_state_all(blob)
-    ctx.cph_step(1000)
+    ctx.cph_step(5000)        # 10 ps under Bussi before sampling: tau_lambda = 1 ps over 3 degrees of freedom
     ka, kl = [], []
     for _ in range(100):
         ctx.cph_step(40)
